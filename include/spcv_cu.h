@@ -1,0 +1,121 @@
+/*
+ * spcv_cu.h — C-ABI boundary of the B200 sparse 1x1-conv SpMM.
+ *
+ * This is the drop-in for the reference's hot path
+ *   spcv::spmm_into / spcv::spmm / spcv::spconv_1x1
+ *   (/root/reference/proj/include/spcv/kernels.hpp:45-55,
+ *    implementation /root/reference/proj/src/kernels.cpp:304-341)
+ * consuming the reference's BCSR weight format
+ *   spcv::BcsrMatrix (/root/reference/proj/include/spcv/sparse.hpp:65-79).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary and
+ * no exception escapes it. Every entry point returns an spcv_status; the
+ * message for the last failure on the calling thread is spcv_cu_last_error().
+ * The C++ mirror of the reference API (include/spcv_b200/spcv.hpp) maps the
+ * codes back onto the reference's exception classes.
+ *
+ * Arithmetic contract: SPCV_MODE_STRICT reproduces the reference per-element
+ * order (bias first, stored blocks in ascending position, separate multiply
+ * and add, ternary clamp) and is bit-exact against the reference CPU kernel.
+ * SPCV_MODE_FAST contracts multiply+add into FFMA and is within the
+ * nnz-scaled 1e-5 tolerance of BASELINE.json's north_star.
+ */
+#ifndef SPCV_CU_H
+#define SPCV_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The numbering is shared with the CPU checkers in oracle/. */
+typedef enum spcv_status {
+    SPCV_OK = 0,
+    SPCV_ERR_LAYOUT = 1,   /* spcv::LayoutError      (tensor.hpp:18-21)   */
+    SPCV_ERR_SHAPE = 2,    /* spcv::ShapeError       (tensor.hpp:12-15)   */
+    SPCV_ERR_FORMAT = 3,   /* spcv::FormatError      (sparse.hpp:12-15)   */
+    SPCV_ERR_INVALID = 4,  /* std::invalid_argument  (kernels.cpp:321-322) */
+    SPCV_ERR_CUDA = 5,     /* CUDA runtime failure (no device, launch error, ...) */
+    SPCV_ERR_UNSUPPORTED = 6 /* shape beyond this build's device limits */
+} spcv_status;
+
+/* Tensor layouts, as spcv::Layout (tensor.hpp:23-26). */
+enum { SPCV_LAYOUT_CHW = 0, SPCV_LAYOUT_HWC = 1 };
+
+/* Fused activation kinds, as spcv::Activation::Kind (tensor.hpp:74-97).
+ * SPCV_ACT_CLAMP requires lo < hi (tensor.hpp:80-81). ReLU = clamp(0, +inf),
+ * ReLU6 = clamp(0, 6). */
+enum { SPCV_ACT_NONE = 0, SPCV_ACT_CLAMP = 1 };
+
+/* Arithmetic modes. */
+enum { SPCV_MODE_STRICT = 0, SPCV_MODE_FAST = 1 };
+
+/* Opaque device-resident packed weights (one BcsrMatrix, one device). */
+typedef struct spcv_cu_weights spcv_cu_weights;
+
+/* Pack a reference BcsrMatrix (host arrays, exactly the fields of
+ * sparse.hpp:65-79) into device-resident streams on the current CUDA device:
+ * per-block-row nnz counts, per-block input-channel deltas and the block
+ * values (the paper's format), plus the row-bucketed execution schedule.
+ * The matrix is validated with the checks of BcsrMatrix::validate
+ * (sparse.cpp:16-51); a malformed matrix yields SPCV_ERR_FORMAT.
+ * Replaces: the per-call use of `const BcsrMatrix& w` in spmm_into
+ * (kernels.cpp:304). */
+int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t row_ptr_len,
+                 const uint32_t* col_idx, size_t nblocks, const float* values, size_t nvalues,
+                 spcv_cu_weights** out);
+
+/* Decode the device streams back into BCSR host arrays (row_ptr has
+ * rows/block_h+1 entries, col_idx nblocks, values nblocks*block_h). The
+ * decode runs on the device and is bit-exact: pack followed by unpack
+ * reproduces the input arrays byte for byte. */
+int spcv_cu_unpack(const spcv_cu_weights* w, uint32_t* row_ptr, uint32_t* col_idx,
+                   float* values);
+
+/* Shape of packed weights; any out-pointer may be NULL. */
+int spcv_cu_weights_info(const spcv_cu_weights* w, int* rows, int* cols, int* block_h,
+                         size_t* nblocks, int* row_slots, int* device);
+
+void spcv_cu_free(spcv_cu_weights* w);
+
+/* spmm_into over a batch of `images` CHW images on device memory:
+ *   act [images][act_c][act_h*act_w], out [images][out_c][out_h*out_w].
+ *   out[i][c][s] = fused(bias[c] + sum over c's stored blocks of value*act[i][col][s])
+ * Checks, in the reference order (kernels.cpp:306-322): clamp lo<hi
+ * (tensor.hpp:80-81) -> act layout CHW (LayoutError) -> w.cols == act_c
+ * (ShapeError) -> cfg_n == block_h (FormatError) -> bias_len == 0 or rows
+ * (ShapeError) -> out CHW with out_c == rows and out spatial == act spatial
+ * (ShapeError) -> cfg_m in {0,4,8,16} (invalid_argument). cfg_m is the CPU
+ * strip width; it is validated and otherwise ignored (one CUDA path). bias may
+ * be NULL (bias_len 0) meaning +0.0 (kernels.cpp:21,110). Asynchronous on
+ * `stream` (a cudaStream_t, NULL = legacy default stream). */
+int spcv_cu_spmm_into(const spcv_cu_weights* w, const float* act, int act_layout, int images,
+                      int act_c, int act_h, int act_w, const float* bias, size_t bias_len,
+                      int act_kind, float lo, float hi, float* out, int out_layout, int out_c,
+                      int out_h, int out_w, int cfg_m, int cfg_n, int mode, void* stream);
+
+/* Same contract with HOST act/bias/out buffers: host->device copy, kernel,
+ * device->host copy, synchronous. This is the reference-facing call shape
+ * (spmm_into with host Tensors). Pinned host buffers give full PCIe speed. */
+int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_layout,
+                           int images, int act_c, int act_h, int act_w, const float* bias,
+                           size_t bias_len, int act_kind, float lo, float hi, float* out,
+                           int out_layout, int out_c, int out_h, int out_w, int cfg_m, int cfg_n,
+                           int mode);
+
+/* Number of SpMM kernel launches issued by this library so far (process-wide). */
+uint64_t spcv_cu_launch_count(void);
+
+/* Message describing the last failure on the calling thread ("" if none). */
+const char* spcv_cu_last_error(void);
+
+/* Library build string (arch, version). */
+const char* spcv_cu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPCV_CU_H */

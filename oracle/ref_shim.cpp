@@ -1,0 +1,217 @@
+// ref_shim.cpp — extern "C" entry points over the UNMODIFIED reference library.
+//
+// TEST/BASELINE INFRASTRUCTURE ONLY. oracle/Makefile compiles this file together
+// with /root/reference/proj/src/{tensor,sparse,kernels}.cpp (read in place,
+// never copied) into oracle/_ref/libspcv_ref.so. Tests use it to pin the
+// oracle restatement; bench.py uses it as the CPU baseline ("kind":
+// "reference") and as the `--impl reference` arm.
+//
+// Error mapping (same codes as include/spcv_cu.h):
+//   LayoutError -> 1, ShapeError -> 2, FormatError -> 3,
+//   other std::invalid_argument -> 4, anything else -> 5.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "spcv/kernels.hpp"
+#include "spcv/sparse.hpp"
+#include "spcv/tensor.hpp"
+
+namespace {
+
+int code_of(const std::exception_ptr& e) {
+    try {
+        std::rethrow_exception(e);
+    } catch (const spcv::LayoutError&) {
+        return 1;
+    } catch (const spcv::ShapeError&) {
+        return 2;
+    } catch (const spcv::FormatError&) {
+        return 3;
+    } catch (const std::invalid_argument&) {
+        return 4;
+    } catch (...) {
+        return 5;
+    }
+}
+
+spcv::BcsrMatrix make_bcsr(int rows, int cols, int block_h, const std::uint32_t* row_ptr,
+                           std::size_t nrp, const std::uint32_t* col_idx, std::size_t nblk,
+                           const float* values, std::size_t nval) {
+    spcv::BcsrMatrix m;
+    m.rows = rows;
+    m.cols = cols;
+    m.block_h = block_h;
+    m.row_ptr.assign(row_ptr, row_ptr + nrp);
+    m.col_idx.assign(col_idx, col_idx + nblk);
+    m.values.assign(values, values + nval);
+    return m;
+}
+
+spcv::Activation make_act(int kind, float lo, float hi) {
+    return kind == 0 ? spcv::Activation::none() : spcv::Activation::clamp(lo, hi);
+}
+
+spcv::Tier tier_of(int t) {
+    return t == 0 ? spcv::Tier::Scalar : (t == 1 ? spcv::Tier::Vector : spcv::Tier::Auto);
+}
+
+}  // namespace
+
+extern "C" {
+
+// spcv::spmm_into over `images` independent CHW images (act [images][cols][H*W],
+// out [images][rows][H*W]). act_layout 1 = HWC (to exercise LayoutError).
+int ref_spmm(int rows, int cols, int block_h, const std::uint32_t* row_ptr, std::size_t nrp,
+             const std::uint32_t* col_idx, std::size_t nblk, const float* values,
+             std::size_t nval, int images, int act_channels, int H, int W, int act_layout,
+             const float* act, const float* bias, std::size_t bias_len, int act_kind, float lo,
+             float hi, int out_channels, float* out, int cfg_m, int cfg_n, int prefetch,
+             int tier) {
+    try {
+        const spcv::BcsrMatrix m =
+            make_bcsr(rows, cols, block_h, row_ptr, nrp, col_idx, nblk, values, nval);
+        const spcv::Activation fn = make_act(act_kind, lo, hi);
+        spcv::MicrokernelConfig cfg;
+        cfg.m = cfg_m;
+        cfg.n = cfg_n;
+        cfg.prefetch = prefetch != 0;
+        cfg.tier = tier_of(tier);
+        const std::size_t in_sz = static_cast<std::size_t>(act_channels) * H * W;
+        const std::size_t out_sz = static_cast<std::size_t>(out_channels) * H * W;
+        std::span<const float> b(bias, bias ? bias_len : 0);
+        for (int i = 0; i < images; ++i) {
+            spcv::Tensor a(act_channels, H, W,
+                           act_layout == 1 ? spcv::Layout::HWC : spcv::Layout::CHW);
+            std::memcpy(a.data.data(), act + i * in_sz, in_sz * sizeof(float));
+            spcv::Tensor o(out_channels, H, W, spcv::Layout::CHW);
+            spcv::spmm_into(m, a, b, fn, o, cfg);
+            std::memcpy(out + i * out_sz, o.data.data(), out_sz * sizeof(float));
+        }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+int ref_matmul_reference(int rows, int cols, int H, int W, const float* w, const float* act,
+                         const float* bias, int act_kind, float lo, float hi, float* out) {
+    try {
+        spcv::DenseMatrix dm(rows, cols);
+        std::memcpy(dm.data.data(), w, sizeof(float) * dm.data.size());
+        spcv::Tensor a(cols, H, W, spcv::Layout::CHW);
+        std::memcpy(a.data.data(), act, sizeof(float) * a.data.size());
+        std::span<const float> b(bias, bias ? static_cast<std::size_t>(rows) : 0);
+        const spcv::Tensor o = spcv::matmul_reference(dm, a, b, make_act(act_kind, lo, hi));
+        std::memcpy(out, o.data.data(), sizeof(float) * o.data.size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+int ref_encode_bcsr(int rows, int cols, int block_h, const float* w, std::uint32_t* row_ptr,
+                    std::uint32_t* col_idx, float* values, std::size_t* nblocks) {
+    try {
+        spcv::DenseMatrix dm(rows, cols);
+        std::memcpy(dm.data.data(), w, sizeof(float) * dm.data.size());
+        const spcv::BcsrMatrix m = spcv::encode_bcsr(dm, block_h);
+        std::copy(m.row_ptr.begin(), m.row_ptr.end(), row_ptr);
+        std::copy(m.col_idx.begin(), m.col_idx.end(), col_idx);
+        std::copy(m.values.begin(), m.values.end(), values);
+        *nblocks = m.col_idx.size();
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+int ref_validate_bcsr(int rows, int cols, int block_h, const std::uint32_t* row_ptr,
+                      std::size_t nrp, const std::uint32_t* col_idx, std::size_t nblk,
+                      const float* values, std::size_t nval) {
+    try {
+        make_bcsr(rows, cols, block_h, row_ptr, nrp, col_idx, nblk, values, nval).validate();
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+int ref_generate_mask(int rows, int cols, double sparsity, int out_block, int in_block,
+                      std::uint32_t seed, std::uint8_t* keep) {
+    try {
+        const spcv::SparsityMask mk =
+            spcv::generate_mask(rows, cols, sparsity, spcv::BlockConfig(out_block, in_block), seed);
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c)
+                keep[static_cast<std::size_t>(r) * cols + c] = mk.get(r, c) ? 1 : 0;
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// Timed CPU baseline: spmm_into over `images` images split contiguously over
+// `nthreads` std::threads (reentrant per /root/reference/SPEC.md:290), default
+// MicrokernelConfig with n = block_h (Auto tier -> vector, 16xN strips).
+// Tensors are built once outside the timed region. Runs `warmups` untimed
+// passes then `reps` timed passes; writes the per-pass seconds to secs[reps].
+int ref_bench_spmm(int rows, int cols, int block_h, const std::uint32_t* row_ptr,
+                   std::size_t nrp, const std::uint32_t* col_idx, std::size_t nblk,
+                   const float* values, std::size_t nval, int images, int H, int W,
+                   const float* act, const float* bias, int act_kind, float lo, float hi,
+                   float* out, int nthreads, int warmups, int reps, double* secs) {
+    try {
+        const spcv::BcsrMatrix m =
+            make_bcsr(rows, cols, block_h, row_ptr, nrp, col_idx, nblk, values, nval);
+        const spcv::Activation fn = make_act(act_kind, lo, hi);
+        spcv::MicrokernelConfig cfg;
+        cfg.n = block_h;
+        const std::size_t in_sz = static_cast<std::size_t>(cols) * H * W;
+        const std::size_t out_sz = static_cast<std::size_t>(rows) * H * W;
+        std::vector<spcv::Tensor> ins, outs;
+        ins.reserve(images);
+        outs.reserve(images);
+        for (int i = 0; i < images; ++i) {
+            ins.emplace_back(cols, H, W, spcv::Layout::CHW);
+            std::memcpy(ins.back().data.data(), act + i * in_sz, in_sz * sizeof(float));
+            outs.emplace_back(rows, H, W, spcv::Layout::CHW);
+        }
+        std::span<const float> b(bias, bias ? static_cast<std::size_t>(rows) : 0);
+        if (nthreads < 1) nthreads = 1;
+        nthreads = std::min(nthreads, std::max(images, 1));
+        auto pass = [&] {
+            std::vector<std::thread> th;
+            th.reserve(nthreads);
+            for (int t = 0; t < nthreads; ++t) {
+                const int i0 = static_cast<int>(static_cast<long>(images) * t / nthreads);
+                const int i1 = static_cast<int>(static_cast<long>(images) * (t + 1) / nthreads);
+                th.emplace_back([&, i0, i1] {
+                    for (int i = i0; i < i1; ++i) spcv::spmm_into(m, ins[i], b, fn, outs[i], cfg);
+                });
+            }
+            for (auto& t : th) t.join();
+        };
+        for (int i = 0; i < warmups; ++i) pass();
+        for (int r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            pass();
+            const auto t1 = std::chrono::steady_clock::now();
+            secs[r] = std::chrono::duration<double>(t1 - t0).count();
+        }
+        if (out)
+            for (int i = 0; i < images; ++i)
+                std::memcpy(out + i * out_sz, outs[i].data.data(), out_sz * sizeof(float));
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+}  // extern "C"

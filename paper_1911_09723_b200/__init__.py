@@ -1,0 +1,40 @@
+"""paper_1911_09723_b200 — B200-native sparse 1x1-convolution SpMM.
+
+A drop-in for the reference ``spcv::spmm_into`` hot path
+(/root/reference/proj/src/kernels.cpp:304-334) built on hand-written sm_100a
+kernels behind the C-ABI in ``include/spcv_cu.h``. See DESIGN.md.
+"""
+from ._capi import LIB_PATH, launch_count
+from .spmm import (
+    Activation,
+    BcsrMatrix,
+    DeviceBcsr,
+    DeviceError,
+    FormatError,
+    Layout,
+    LayoutError,
+    MicrokernelConfig,
+    ShapeError,
+    Tensor,
+    Tier,
+    decode_bcsr,
+    default_strip_width,
+    encode_bcsr,
+    parse_tier,
+    parse_variant,
+    resolve_tier,
+    spconv_1x1,
+    spmm,
+    spmm_batched_into,
+    spmm_host_batched,
+    spmm_into,
+    variant_name,
+)
+
+__all__ = [
+    "Activation", "BcsrMatrix", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
+    "LayoutError", "MicrokernelConfig", "ShapeError", "Tensor", "Tier", "decode_bcsr",
+    "default_strip_width", "encode_bcsr", "parse_tier", "parse_variant", "resolve_tier",
+    "spconv_1x1", "spmm", "spmm_batched_into", "spmm_host_batched", "spmm_into",
+    "variant_name", "launch_count", "LIB_PATH",
+]

@@ -1,0 +1,60 @@
+"""ctypes binding of the C-ABI in include/spcv_cu.h (lib/libspcv_cu.so).
+
+The shared library is built in-tree by ``paper_1911_09723_b200.build`` (or
+``__graft_entry__.build()``). There is no fallback: if the library is missing
+or cannot be loaded, importing this module raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libspcv_cu.so")
+
+# spcv_status (include/spcv_cu.h)
+OK, ERR_LAYOUT, ERR_SHAPE, ERR_FORMAT, ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+LAYOUT_CHW, LAYOUT_HWC = 0, 1
+ACT_NONE, ACT_CLAMP = 0, 1
+MODE_STRICT, MODE_FAST = 0, 1
+
+# Every symbol include/spcv_cu.h declares, with (restype, argtypes).
+_p, _i, _f, _z, _u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t, ctypes.c_uint64
+_SPMM_ARGS = [_p, _p, _i, _i, _i, _i, _i, _p, _z, _i, _f, _f, _p, _i, _i, _i, _i, _i, _i, _i]
+SIGNATURES = {
+    "spcv_cu_pack": (_i, [_i, _i, _i, _p, _z, _p, _z, _p, _z, ctypes.POINTER(_p)]),
+    "spcv_cu_unpack": (_i, [_p, _p, _p, _p]),
+    "spcv_cu_weights_info": (_i, [_p, _p, _p, _p, _p, _p, _p]),
+    "spcv_cu_free": (None, [_p]),
+    "spcv_cu_spmm_into": (_i, _SPMM_ARGS + [_p]),
+    "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
+    "spcv_cu_launch_count": (_u64, []),
+    "spcv_cu_last_error": (ctypes.c_char_p, []),
+    "spcv_cu_version": (ctypes.c_char_p, []),
+}
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    msg = lib.spcv_cu_last_error()
+    return msg.decode() if msg else ""
+
+
+def launch_count() -> int:
+    return int(lib.spcv_cu_launch_count())

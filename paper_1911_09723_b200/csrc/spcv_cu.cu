@@ -1,0 +1,539 @@
+// spcv_cu.cu — C-ABI shim (include/spcv_cu.h): weight packing, argument
+// checks in the reference order, kernel selection and launch.
+//
+// Reference interface replaced: spcv::spmm_into (kernels.hpp:45-46,
+// kernels.cpp:304-334) and the BcsrMatrix it consumes (sparse.hpp:65-79).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <queue>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/spcv_cu.h"
+#include "spmm_kernel.cuh"
+
+using spcvk::kBins;
+using spcvk::kMaxSplit;
+using spcvk::kThreads;
+using spcvk::kWarps;
+
+struct spcv_cu_weights {
+    int rows = 0, cols = 0, block_h = 1, brows = 0;
+    int G = 1;           // block rows per warp group
+    int T = 128;         // virtual columns per tile
+    int device = 0;
+    size_t nblocks = 0;
+    size_t nchunks = 0;
+    // paper-format streams (north_star): counts, deltas, values
+    uint32_t* d_nnz = nullptr;
+    uint32_t* d_delta = nullptr;
+    float* d_values = nullptr;
+    // execution schedule
+    uint4* d_stream = nullptr;
+    uint32_t* d_bin_beg = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SPCV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define SPCV_CUDA(call)                                  \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+constexpr size_t kSmemLimit = 227 * 1024;
+constexpr size_t kTwoCtaSmem = 112 * 1024;
+
+// Smallest G (block rows per warp) whose [K][T] tile (+ bias) fits the budget.
+// G=1 -> T=128, G=2 -> T=64, G=4 -> T=32 columns. Prefer two CTAs per SM.
+int choose_groups(int K, int M) {
+    for (int G : {1, 2, 4}) {
+        const size_t smem = static_cast<size_t>(K) * (128 / G) * 4 + static_cast<size_t>(M) * 4;
+        if (smem <= kTwoCtaSmem) return G;
+    }
+    const size_t smem4 = static_cast<size_t>(K) * 32 * 4 + static_cast<size_t>(M) * 4;
+    return smem4 <= kSmemLimit ? 4 : 0;
+}
+
+int bitrev3(int i) { return ((i & 1) << 2) | (i & 2) | ((i & 4) >> 2); }
+
+struct DevProps {
+    int sms = 148;
+};
+
+DevProps props_for(int dev) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, DevProps>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& p : cache)
+        if (p.first == dev) return p.second;
+    DevProps d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cache.emplace_back(dev, d);
+    return d;
+}
+
+template <typename T>
+int upload(T** dst, const T* src, size_t n) {
+    *dst = nullptr;
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    SPCV_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), bytes));
+    if (n) SPCV_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    return SPCV_OK;
+}
+
+void free_weights(spcv_cu_weights* w) {
+    if (!w) return;
+    cudaFree(w->d_nnz);
+    cudaFree(w->d_delta);
+    cudaFree(w->d_values);
+    cudaFree(w->d_stream);
+    cudaFree(w->d_bin_beg);
+    delete w;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ packing
+
+extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row_ptr,
+                            size_t row_ptr_len, const uint32_t* col_idx, size_t nblocks,
+                            const float* values, size_t nvalues, spcv_cu_weights** out) {
+    g_last_error.clear();
+    if (!out) return fail(SPCV_ERR_INVALID, "spcv_cu_pack: out is null");
+    *out = nullptr;
+    // BcsrMatrix::validate (sparse.cpp:16-51), same checks, same order.
+    if (rows < 1 || cols < 1) return fail(SPCV_ERR_FORMAT, "bcsr: dims must be >= 1");
+    if (block_h != 1 && block_h != 2 && block_h != 4)
+        return fail(SPCV_ERR_FORMAT, "bcsr: block height must be 1, 2 or 4");
+    if (rows % block_h != 0)
+        return fail(SPCV_ERR_FORMAT, "bcsr: rows " + std::to_string(rows) +
+                                         " not divisible by block height " +
+                                         std::to_string(block_h));
+    const int brows = rows / block_h;
+    if (row_ptr_len != static_cast<size_t>(brows) + 1 || !row_ptr)
+        return fail(SPCV_ERR_FORMAT, "bcsr: row_ptr length != block rows + 1");
+    if (row_ptr[0] != 0) return fail(SPCV_ERR_FORMAT, "bcsr: row_ptr[0] != 0");
+    for (int r = 0; r < brows; ++r)
+        if (row_ptr[r] > row_ptr[r + 1])
+            return fail(SPCV_ERR_FORMAT,
+                        "bcsr: row_ptr not non-decreasing at block row " + std::to_string(r));
+    if (row_ptr[brows] != nblocks)
+        return fail(SPCV_ERR_FORMAT, "bcsr: row_ptr[-1] != block count");
+    if (nvalues != nblocks * static_cast<size_t>(block_h))
+        return fail(SPCV_ERR_FORMAT, "bcsr: values length != block count * block height");
+    if (nblocks && (!col_idx || !values)) return fail(SPCV_ERR_FORMAT, "bcsr: null arrays");
+    for (int r = 0; r < brows; ++r) {
+        for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
+            if (col_idx[b] >= static_cast<uint32_t>(cols))
+                return fail(SPCV_ERR_FORMAT, "bcsr: column index " + std::to_string(col_idx[b]) +
+                                                 " out of range in block row " + std::to_string(r));
+            if (b > row_ptr[r] && col_idx[b] <= col_idx[b - 1])
+                return fail(SPCV_ERR_FORMAT,
+                            "bcsr: column indices not strictly increasing in block row " +
+                                std::to_string(r));
+        }
+    }
+
+    const int G = choose_groups(cols, rows);
+    if (G == 0)
+        return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: input channels " + std::to_string(cols) +
+                                              " exceed the shared-memory tile limit");
+    const int T = 128 / G;
+    const uint32_t pitch = static_cast<uint32_t>(T) * 4;  // smem bytes per activation row
+    const int BH = block_h;
+
+    // paper-format streams
+    std::vector<uint32_t> nnz(brows), delta(nblocks);
+    for (int r = 0; r < brows; ++r) {
+        nnz[r] = row_ptr[r + 1] - row_ptr[r];
+        uint32_t prev = 0;
+        for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
+            delta[b] = col_idx[b] - prev;
+            prev = col_idx[b];
+        }
+    }
+
+    // Row bucketing: sort block rows by nnz (descending), form groups of G
+    // neighbours (similar lengths -> little predication), then LPT the groups
+    // over kBins bins. Bin b = warp*kMaxSplit + i; ties go to the bin whose
+    // (bit-reversed i, warp) is smallest so every split level stays balanced.
+    std::vector<int> order(brows);
+    for (int r = 0; r < brows; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return nnz[a] > nnz[b]; });
+    const int ngroups = (brows + G - 1) / G;
+    std::vector<int> gchunks(ngroups);
+    for (int g = 0; g < ngroups; ++g) {
+        uint32_t mx = 0;
+        for (int s = 0; s < G; ++s) {
+            const int k = g * G + s;
+            if (k < brows) mx = std::max(mx, nnz[order[k]]);
+        }
+        gchunks[g] = static_cast<int>((mx + 3) / 4);
+    }
+    std::vector<std::vector<int>> bins(kBins);
+    using Item = std::tuple<long long, int, int>;  // load, priority, bin
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int b = 0; b < kBins; ++b) {
+        const int warp = b / kMaxSplit, i = b % kMaxSplit;
+        heap.emplace(0LL, bitrev3(i) * kWarps + warp, b);
+    }
+    std::vector<int> gorder(ngroups);
+    for (int g = 0; g < ngroups; ++g) gorder[g] = g;
+    std::stable_sort(gorder.begin(), gorder.end(),
+                     [&](int a, int b) { return gchunks[a] > gchunks[b]; });
+    for (int g : gorder) {
+        auto [load, prio, b] = heap.top();
+        heap.pop();
+        bins[b].push_back(g);
+        heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
+    }
+
+    const int CH = G * (1 + BH);  // 16 B units per chunk
+    size_t total = 0;
+    for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
+    std::vector<uint4> stream(total * CH, make_uint4(0, 0, 0, 0));
+    std::vector<uint32_t> bin_beg(kBins + 1);
+    size_t cur = 0;
+    for (int b = 0; b < kBins; ++b) {
+        bin_beg[b] = static_cast<uint32_t>(cur);
+        for (int g : bins[b]) {
+            const int nch = gchunks[g];
+            uint4* hdr = stream.data() + cur * CH;
+            for (int s = 0; s < G; ++s) {
+                const int k = g * G + s;
+                if (k < brows) {
+                    const int br = order[k];
+                    hdr[s] = make_uint4(static_cast<uint32_t>(br), nnz[br],
+                                        static_cast<uint32_t>(nch), 0u);
+                } else {
+                    hdr[s] = make_uint4(0xFFFFFFFFu, 0u, static_cast<uint32_t>(nch), 0u);
+                }
+            }
+            ++cur;
+            for (int c = 0; c < nch; ++c, ++cur) {
+                uint4* ch = stream.data() + cur * CH;
+                for (int s = 0; s < G; ++s) {
+                    const int k = g * G + s;
+                    if (k >= brows) continue;
+                    const int br = order[k];
+                    uint32_t off[4] = {0, 0, 0, 0};
+                    float vals[16] = {0};
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t e = static_cast<uint32_t>(4 * c + t);
+                        if (e >= nnz[br]) continue;
+                        const uint32_t blk = row_ptr[br] + e;
+                        off[t] = col_idx[blk] * pitch;
+                        for (int i = 0; i < BH; ++i)
+                            vals[t * BH + i] = values[static_cast<size_t>(blk) * BH + i];
+                    }
+                    ch[s] = make_uint4(off[0], off[1], off[2], off[3]);
+                    for (int j = 0; j < BH; ++j) {
+                        uint4 u;
+                        std::memcpy(&u, vals + 4 * j, 16);
+                        ch[G + j * G + s] = u;
+                    }
+                }
+            }
+        }
+    }
+    bin_beg[kBins] = static_cast<uint32_t>(cur);
+    if (cur > 0xFFFFFFF0ull) return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: stream too large");
+
+    auto* w = new (std::nothrow) spcv_cu_weights;
+    if (!w) return fail(SPCV_ERR_CUDA, "spcv_cu_pack: out of host memory");
+    w->rows = rows;
+    w->cols = cols;
+    w->block_h = block_h;
+    w->brows = brows;
+    w->G = G;
+    w->T = T;
+    w->nblocks = nblocks;
+    w->nchunks = cur;
+    cudaGetDevice(&w->device);
+    int rc = SPCV_OK;
+    if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
+        (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
+        (rc = upload(&w->d_values, values, nvalues)) ||
+        (rc = upload(&w->d_stream, stream.data(), stream.size())) ||
+        (rc = upload(&w->d_bin_beg, bin_beg.data(), bin_beg.size()))) {
+        free_weights(w);
+        return rc;
+    }
+    *out = w;
+    return SPCV_OK;
+}
+
+extern "C" int spcv_cu_unpack(const spcv_cu_weights* w, uint32_t* row_ptr, uint32_t* col_idx,
+                              float* values) {
+    g_last_error.clear();
+    if (!w || !row_ptr || (w->nblocks && (!col_idx || !values)))
+        return fail(SPCV_ERR_INVALID, "spcv_cu_unpack: null argument");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    SPCV_CUDA(cudaSetDevice(w->device));
+    uint32_t *d_rp = nullptr, *d_ci = nullptr;
+    int rc = SPCV_OK;
+    cudaError_t e = cudaMalloc(&d_rp, sizeof(uint32_t) * (w->brows + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&d_ci, sizeof(uint32_t) * std::max<size_t>(w->nblocks, 1));
+    if (e == cudaSuccess) {
+        spcvk::unpack_rowptr_kernel<<<1, 1>>>(w->d_nnz, w->brows, d_rp);
+        spcvk::unpack_cols_kernel<<<(w->brows + 127) / 128, 128>>>(d_rp, w->d_delta, w->brows, d_ci);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpy(row_ptr, d_rp, sizeof(uint32_t) * (w->brows + 1), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && w->nblocks)
+        e = cudaMemcpy(col_idx, d_ci, sizeof(uint32_t) * w->nblocks, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && w->nblocks)
+        e = cudaMemcpy(values, w->d_values, sizeof(float) * w->nblocks * w->block_h,
+                       cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "spcv_cu_unpack");
+    cudaFree(d_rp);
+    cudaFree(d_ci);
+    cudaSetDevice(prev);
+    return rc;
+}
+
+extern "C" int spcv_cu_weights_info(const spcv_cu_weights* w, int* rows, int* cols, int* block_h,
+                                    size_t* nblocks, int* row_slots, int* device) {
+    if (!w) return fail(SPCV_ERR_INVALID, "spcv_cu_weights_info: null weights");
+    if (rows) *rows = w->rows;
+    if (cols) *cols = w->cols;
+    if (block_h) *block_h = w->block_h;
+    if (nblocks) *nblocks = w->nblocks;
+    if (row_slots) *row_slots = w->G;
+    if (device) *device = w->device;
+    return SPCV_OK;
+}
+
+extern "C" void spcv_cu_free(spcv_cu_weights* w) { free_weights(w); }
+
+// ------------------------------------------------------------------- launch
+
+namespace {
+
+template <int BH, int G, bool STRICT, bool VEC>
+int launch_one(const spcvk::KernelArgs& a, long long ntiles, int split, size_t smem,
+               cudaStream_t st) {
+    auto kern = spcvk::spmm_bcsr_kernel<BH, G, STRICT, VEC>;
+    // cudaFuncSetAttribute is per device; remember which devices are done.
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSmemLimit)));
+        configured.fetch_or(bit);
+    }
+    (void)smem;
+    dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(split));
+    kern<<<grid, kThreads, smem, st>>>(a);
+    SPCV_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SPCV_OK;
+}
+
+template <int BH, int G>
+int launch_g(const spcvk::KernelArgs& a, long long ntiles, int split, size_t smem, bool strict,
+             bool vec, cudaStream_t st) {
+    if (strict)
+        return vec ? launch_one<BH, G, true, true>(a, ntiles, split, smem, st)
+                   : launch_one<BH, G, true, false>(a, ntiles, split, smem, st);
+    return vec ? launch_one<BH, G, false, true>(a, ntiles, split, smem, st)
+               : launch_one<BH, G, false, false>(a, ntiles, split, smem, st);
+}
+
+template <int BH>
+int launch_bh(const spcvk::KernelArgs& a, int G, long long ntiles, int split, size_t smem,
+              bool strict, bool vec, cudaStream_t st) {
+    switch (G) {
+        case 1: return launch_g<BH, 1>(a, ntiles, split, smem, strict, vec, st);
+        case 2: return launch_g<BH, 2>(a, ntiles, split, smem, strict, vec, st);
+        default: return launch_g<BH, 4>(a, ntiles, split, smem, strict, vec, st);
+    }
+}
+
+// Argument checks in the order of spmm_into (kernels.cpp:306-322).
+int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, int act_h,
+               int act_w, size_t bias_len, int act_kind, float lo, float hi, int out_layout,
+               int out_c, int out_h, int out_w, int cfg_m, int cfg_n, int mode) {
+    if (!w) return fail(SPCV_ERR_INVALID, "spmm: null weights");
+    if (act_kind != SPCV_ACT_NONE && act_kind != SPCV_ACT_CLAMP)
+        return fail(SPCV_ERR_INVALID, "spmm: unknown activation kind");
+    if (act_kind == SPCV_ACT_CLAMP && !(lo < hi))
+        return fail(SPCV_ERR_INVALID, "clamp requires lo < hi");
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "spmm: unknown arithmetic mode");
+    if (act_layout != SPCV_LAYOUT_CHW) return fail(SPCV_ERR_LAYOUT, "spmm: activation must be CHW");
+    if (w->cols != act_c)
+        return fail(SPCV_ERR_SHAPE, "spmm: weight cols " + std::to_string(w->cols) +
+                                        " != activation channels " + std::to_string(act_c));
+    if (cfg_n != w->block_h)
+        return fail(SPCV_ERR_FORMAT, "spmm: cfg out_block " + std::to_string(cfg_n) +
+                                         " != matrix block height " + std::to_string(w->block_h));
+    if (bias_len != 0 && bias_len != static_cast<size_t>(w->rows))
+        return fail(SPCV_ERR_SHAPE, "spmm: bias length != rows");
+    if (out_layout != SPCV_LAYOUT_CHW || out_c != w->rows || out_h != act_h || out_w != act_w)
+        return fail(SPCV_ERR_SHAPE, "spmm: output tensor shape/layout mismatch");
+    if (cfg_m != 0 && cfg_m != 4 && cfg_m != 8 && cfg_m != 16)
+        return fail(SPCV_ERR_INVALID, "spmm: strip width must be 4, 8 or 16");
+    if (images < 0 || act_h < 1 || act_w < 1)
+        return fail(SPCV_ERR_SHAPE, "spmm: tensor dims must be >= 1");
+    return SPCV_OK;
+}
+
+int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, int act_w,
+           const float* bias, int act_kind, float lo, float hi, float* out, int mode,
+           cudaStream_t st) {
+    const long long S = static_cast<long long>(act_h) * act_w;
+    const long long N = S * images;
+    if (N == 0) return SPCV_OK;
+    if (S > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: spatial extent too large");
+    if (!act || !out) return fail(SPCV_ERR_INVALID, "spmm: null tensor pointer");
+    int dev = 0;
+    SPCV_CUDA(cudaGetDevice(&dev));
+    if (dev != w->device)
+        return fail(SPCV_ERR_INVALID, "spmm: weights were packed on device " +
+                                          std::to_string(w->device) + ", current device is " +
+                                          std::to_string(dev));
+    spcvk::KernelArgs a;
+    a.act = act;
+    a.out = out;
+    a.bias = bias;
+    a.stream = w->d_stream;
+    a.bin_beg = w->d_bin_beg;
+    a.N = N;
+    a.K = w->cols;
+    a.M = w->rows;
+    a.S = static_cast<int>(S);
+    a.act_kind = act_kind;
+    a.lo = lo;
+    a.hi = hi;
+    const long long ntiles = (N + w->T - 1) / w->T;
+    if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
+    const size_t smem = static_cast<size_t>(w->cols) * w->T * 4 + static_cast<size_t>(w->rows) * 4;
+    // Row split: CTAs sharing a tile, so small batches still fill the GPU.
+    const int sms = props_for(dev).sms;
+    const int per_sm = (w->block_h == 1 && smem <= kTwoCtaSmem) ? 2 : 1;
+    int split = 1;
+    while (split < kMaxSplit && ntiles * split < static_cast<long long>(sms) * per_sm) split *= 2;
+    const bool vec = (S % 4 == 0) && (reinterpret_cast<uintptr_t>(act) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    const bool strict = mode == SPCV_MODE_STRICT;
+    switch (w->block_h) {
+        case 1: return launch_bh<1>(a, w->G, ntiles, split, smem, strict, vec, st);
+        case 2: return launch_bh<2>(a, w->G, ntiles, split, smem, strict, vec, st);
+        default: return launch_bh<4>(a, w->G, ntiles, split, smem, strict, vec, st);
+    }
+}
+
+struct HostScratch {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    float* buf = nullptr;
+    size_t cap = 0;  // floats
+    ~HostScratch() {
+        if (buf) cudaFree(buf);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+thread_local HostScratch g_scratch;
+
+}  // namespace
+
+extern "C" int spcv_cu_spmm_into(const spcv_cu_weights* w, const float* act, int act_layout,
+                                 int images, int act_c, int act_h, int act_w, const float* bias,
+                                 size_t bias_len, int act_kind, float lo, float hi, float* out,
+                                 int out_layout, int out_c, int out_h, int out_w, int cfg_m,
+                                 int cfg_n, int mode, void* stream) {
+    g_last_error.clear();
+    const int rc = check_args(w, act_layout, images, act_c, act_h, act_w, bias_len, act_kind, lo,
+                              hi, out_layout, out_c, out_h, out_w, cfg_m, cfg_n, mode);
+    if (rc) return rc;
+    return launch(w, act, images, act_h, act_w, bias_len ? bias : nullptr, act_kind, lo, hi, out,
+                  mode, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_layout,
+                                      int images, int act_c, int act_h, int act_w,
+                                      const float* bias, size_t bias_len, int act_kind, float lo,
+                                      float hi, float* out, int out_layout, int out_c, int out_h,
+                                      int out_w, int cfg_m, int cfg_n, int mode) {
+    g_last_error.clear();
+    int rc = check_args(w, act_layout, images, act_c, act_h, act_w, bias_len, act_kind, lo, hi,
+                        out_layout, out_c, out_h, out_w, cfg_m, cfg_n, mode);
+    if (rc) return rc;
+    const size_t S = static_cast<size_t>(act_h) * act_w;
+    const size_t n_in = S * act_c * images, n_out = S * out_c * images;
+    const size_t n_bias = bias_len ? bias_len : 0;
+    if (n_in + n_out == 0) return SPCV_OK;
+    int prev = 0;
+    SPCV_CUDA(cudaGetDevice(&prev));
+    SPCV_CUDA(cudaSetDevice(w->device));
+    HostScratch& hs = g_scratch;
+    if (hs.device != w->device) {
+        if (hs.buf) cudaFree(hs.buf);
+        if (hs.stream) cudaStreamDestroy(hs.stream);
+        hs.buf = nullptr;
+        hs.cap = 0;
+        hs.stream = nullptr;
+        hs.device = w->device;
+        SPCV_CUDA(cudaStreamCreateWithFlags(&hs.stream, cudaStreamNonBlocking));
+    }
+    // 16 B-aligned sub-buffers: act | out | bias
+    auto up4 = [](size_t n) { return (n + 3) & ~static_cast<size_t>(3); };
+    const size_t need = up4(n_in) + up4(n_out) + up4(n_bias);
+    if (need > hs.cap) {
+        if (hs.buf) cudaFree(hs.buf);
+        hs.buf = nullptr;
+        hs.cap = 0;
+        SPCV_CUDA(cudaMalloc(&hs.buf, need * sizeof(float)));
+        hs.cap = need;
+    }
+    float* d_act = hs.buf;
+    float* d_out = d_act + up4(n_in);
+    float* d_bias = n_bias ? d_out + up4(n_out) : nullptr;
+    SPCV_CUDA(cudaMemcpyAsync(d_act, act, n_in * sizeof(float), cudaMemcpyHostToDevice, hs.stream));
+    if (n_bias)
+        SPCV_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice,
+                                  hs.stream));
+    rc = launch(w, d_act, images, act_h, act_w, d_bias, act_kind, lo, hi, d_out, mode, hs.stream);
+    if (rc) {
+        cudaSetDevice(prev);
+        return rc;
+    }
+    SPCV_CUDA(cudaMemcpyAsync(out, d_out, n_out * sizeof(float), cudaMemcpyDeviceToHost, hs.stream));
+    SPCV_CUDA(cudaStreamSynchronize(hs.stream));
+    cudaSetDevice(prev);
+    return SPCV_OK;
+}
+
+extern "C" uint64_t spcv_cu_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char* spcv_cu_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char* spcv_cu_version(void) {
+    return "spcv_cu 0.1 sm_100a (strict+fast, block_h 1/2/4, row slots 1/2/4)";
+}

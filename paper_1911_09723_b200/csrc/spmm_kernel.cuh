@@ -1,0 +1,309 @@
+// spmm_kernel.cuh — sm_100a SpMM kernel for sparse 1x1 convolutions.
+//
+// Replaces the reference strip microkernels spmm_strip_scalar / spmm_strip_vector
+// (/root/reference/proj/src/kernels.cpp:14-43, 101-130) and their strip loop
+// (kernels.cpp:324-333). Same per-element arithmetic:
+//   acc = bias[r]  (or +0.0)                         kernels.cpp:21,110
+//   for stored blocks of r's block row, ascending:   kernels.cpp:25,114
+//       acc += value * act[col][s]                   kernels.cpp:30,120
+//   out = clamp(acc) with the ternary compare        kernels.cpp:38, 93-99
+//
+// B200 mapping:
+//  * The column dimension N = images x H*W ("virtual columns") is cut into
+//    tiles of T = 4*32/G columns; one CTA owns one tile and stages the whole
+//    [K][T] activation block into shared memory once (cp.async, 16 B vectors
+//    when H*W % 4 == 0). Every output row of the tile is then produced from
+//    shared memory, so each activation byte crosses HBM exactly once.
+//  * A warp works on G block rows at a time (a "row group"); each block row
+//    owns 32/G lanes, each lane owns 4 consecutive virtual columns (float4).
+//    One activation LDS.128 per stored block feeds 4*block_h products.
+//  * Weights arrive as a per-warp contiguous chunk stream built by the host
+//    packer (row bucketing + LPT, see spcv_cu.cu). Every chunk is 4 steps of
+//    (smem byte offset, block values) for each of the G rows, interleaved so a
+//    warp-wide 16 B load is a single L1 wavefront; a register ring keeps
+//    kRing chunks in flight to cover L2 latency.
+//  * STRICT uses separately rounded multiply and add (__fmul_rn/__fadd_rn),
+//    reproducing the reference bit-for-bit; !STRICT uses FFMA.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spcvk {
+
+constexpr int kWarps = 16;              // warps per CTA
+constexpr int kThreads = kWarps * 32;   // 512
+constexpr int kRing = 3;                // chunks of weight stream in flight per warp
+constexpr int kBins = 128;              // schedule bins = kWarps x kMaxSplit
+constexpr int kMaxSplit = kBins / kWarps;  // max CTAs sharing one column tile (8)
+
+struct KernelArgs {
+    const float* act;        // [images][K][S]
+    float* out;              // [images][M][S]
+    const float* bias;       // [M] or nullptr
+    const uint4* stream;     // chunk stream, 16 B units
+    const uint32_t* bin_beg; // kBins + 1 chunk offsets
+    long long N;             // images * S
+    int K, M, S;
+    int act_kind;            // 0 none, 1 clamp
+    float lo, hi;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+template <bool STRICT>
+__device__ __forceinline__ float madd(float acc, float w, float a) {
+    if constexpr (STRICT) {
+        return __fadd_rn(acc, __fmul_rn(w, a));
+    } else {
+        return fmaf(w, a, acc);
+    }
+}
+
+// Activation::apply (tensor.hpp:90-96): ternary compare, NaN and -0.0 pass.
+__device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi) {
+    if (kind == 1) v = v < lo ? lo : (v > hi ? hi : v);
+    return v;
+}
+
+template <int BH>
+struct Chunk {
+    uint4 ix;       // 4 smem byte offsets (data) | {block_row, count, nchunks, 0} (header)
+    uint4 v[BH];    // 4 steps x BH values, step-major
+};
+
+template <int BH, int G, bool STRICT, bool VEC>
+__global__ void __launch_bounds__(kThreads, (BH == 1 ? 2 : 1))
+spmm_bcsr_kernel(const KernelArgs a) {
+    constexpr int LPR = 32 / G;       // lanes per block row
+    constexpr int T = LPR * 4;        // virtual columns per tile
+    constexpr int CH = G * (1 + BH);  // chunk size in 16 B units
+
+    extern __shared__ __align__(16) float smem[];
+    float* s_act = smem;                                // [K][T]
+    float* s_bias = smem + static_cast<size_t>(a.K) * T; // [M]
+
+    const int tid = threadIdx.x;
+    const long long n0 = static_cast<long long>(blockIdx.x) * T;
+    const long long KS = static_cast<long long>(a.K) * a.S;
+
+    // ---- stage bias + the [K][T] activation tile (one HBM pass per byte) ----
+    if (a.bias != nullptr)
+        for (int i = tid; i < a.M; i += kThreads) cp_async4(s_bias + i, a.bias + i);
+    if constexpr (VEC) {
+        constexpr int Q = T / 4;              // float4 per tile row
+        constexpr int KSTEP = kThreads / Q;
+        const int q = tid % Q;
+        const long long n = n0 + 4 * q;
+        const bool valid = n < a.N;           // S % 4 == 0: the quad never straddles images
+        long long src = 0;
+        if (valid) {
+            const long long b = n / a.S;
+            src = b * KS + (n - b * a.S);
+        }
+        for (int k = tid / Q; k < a.K; k += KSTEP) {
+            float* dst = s_act + static_cast<size_t>(k) * T + 4 * q;
+            if (valid)
+                cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
+            else
+                *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    } else {
+        constexpr int KSTEP = kThreads / T;
+        const int c = tid % T;
+        const long long n = n0 + c;
+        const bool valid = n < a.N;
+        long long src = 0;
+        if (valid) {
+            const long long b = n / a.S;
+            src = b * KS + (n - b * a.S);
+        }
+        for (int k = tid / T; k < a.K; k += KSTEP) {
+            float* dst = s_act + static_cast<size_t>(k) * T + c;
+            if (valid)
+                cp_async4(dst, a.act + src + static_cast<long long>(k) * a.S);
+            else
+                *dst = 0.f;
+        }
+    }
+
+    // ---- per-lane geometry ----
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int gi = lane / LPR;   // row slot within the group
+    const int li = lane % LPR;   // column quad within the tile
+    const long long nq = n0 + 4 * li;
+    const long long MS = static_cast<long long>(a.M) * a.S;
+    long long obase[VEC ? 1 : 4];
+    bool ovalid[VEC ? 1 : 4];
+    if constexpr (VEC) {
+        ovalid[0] = nq < a.N;
+        obase[0] = 0;
+        if (ovalid[0]) {
+            const long long b = nq / a.S;
+            obase[0] = b * MS + (nq - b * a.S);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long n = nq + j;
+            ovalid[j] = n < a.N;
+            obase[j] = 0;
+            if (ovalid[j]) {
+                const long long b = n / a.S;
+                obase[j] = b * MS + (n - b * a.S);
+            }
+        }
+    }
+
+    // ---- this warp's contiguous slice of the weight stream ----
+    const int split = gridDim.y;            // CTAs sharing this tile (1,2,4,8)
+    const int per = kMaxSplit / split;      // bins per warp
+    const int bin0 = warp * kMaxSplit + blockIdx.y * per;
+    uint32_t pos = __ldg(a.bin_beg + bin0);
+    const uint32_t end = __ldg(a.bin_beg + bin0 + per);
+
+    const uint4* stream = a.stream;
+    auto load = [&](uint32_t c) {
+        Chunk<BH> ch;
+        if (c < end) {
+            const uint4* p = stream + static_cast<size_t>(c) * CH;
+            ch.ix = ldg_stream(p + gi);
+#pragma unroll
+            for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G + j * G + gi);
+        } else {
+            ch.ix = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
+        }
+        return ch;
+    };
+    Chunk<BH> ring[kRing];
+#pragma unroll
+    for (int d = 0; d < kRing; ++d) ring[d] = load(pos + d);
+    auto next = [&]() {
+        const Chunk<BH> cur = ring[0];
+#pragma unroll
+        for (int d = 0; d + 1 < kRing; ++d) ring[d] = ring[d + 1];
+        ring[kRing - 1] = load(pos + kRing);
+        ++pos;
+        return cur;
+    };
+
+    cp_async_wait_all();
+    __syncthreads();
+
+    const char* s_act_lane = reinterpret_cast<const char*>(s_act) + li * 16;
+    const bool have_bias = a.bias != nullptr;
+
+    while (pos < end) {
+        // header chunk: {block_row | ~0u, count, nchunks, 0} per slot
+        const Chunk<BH> h = next();
+        const uint32_t brow = h.ix.x;
+        const int cnt = static_cast<int>(h.ix.y);
+        const int nch = static_cast<int>(h.ix.z);
+        const bool live = brow != 0xFFFFFFFFu;
+
+        float4 acc[BH];
+#pragma unroll
+        for (int i = 0; i < BH; ++i) {
+            const float b = (live && have_bias) ? s_bias[brow * BH + i] : 0.0f;
+            acc[i] = make_float4(b, b, b, b);
+        }
+
+        for (int c = 0; c < nch; ++c) {
+            const Chunk<BH> d = next();
+            const int lim = cnt - 4 * c;
+            const uint32_t off[4] = {d.ix.x, d.ix.y, d.ix.z, d.ix.w};
+            float wv[4 * BH];
+#pragma unroll
+            for (int j = 0; j < BH; ++j) {
+                wv[4 * j + 0] = __uint_as_float(d.v[j].x);
+                wv[4 * j + 1] = __uint_as_float(d.v[j].y);
+                wv[4 * j + 2] = __uint_as_float(d.v[j].z);
+                wv[4 * j + 3] = __uint_as_float(d.v[j].w);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (t < lim) {
+                    const float4 x = *reinterpret_cast<const float4*>(s_act_lane + off[t]);
+#pragma unroll
+                    for (int i = 0; i < BH; ++i) {
+                        const float w = wv[t * BH + i];
+                        acc[i].x = madd<STRICT>(acc[i].x, w, x.x);
+                        acc[i].y = madd<STRICT>(acc[i].y, w, x.y);
+                        acc[i].z = madd<STRICT>(acc[i].z, w, x.z);
+                        acc[i].w = madd<STRICT>(acc[i].w, w, x.w);
+                    }
+                }
+            }
+        }
+
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < BH; ++i) {
+                const long long row = static_cast<long long>(brow) * BH + i;
+                float4 v = acc[i];
+                v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
+                v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
+                v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
+                v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+                if constexpr (VEC) {
+                    if (ovalid[0])
+                        __stcs(reinterpret_cast<float4*>(a.out + obase[0] + row * a.S), v);
+                } else {
+                    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (ovalid[j]) __stcs(a.out + obase[j] + row * a.S, e[j]);
+                }
+            }
+        }
+    }
+}
+
+// Device decode of the paper-format streams (per-block-row nnz counts,
+// per-block input-channel deltas, values) back into BCSR, for the bit-exact
+// pack/unpack round trip. One thread per block row after a serial prefix over
+// counts (block rows <= a few thousand).
+__global__ void unpack_rowptr_kernel(const uint32_t* nnz, int brows, uint32_t* row_ptr) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        uint32_t acc = 0;
+        row_ptr[0] = 0;
+        for (int r = 0; r < brows; ++r) {
+            acc += nnz[r];
+            row_ptr[r + 1] = acc;
+        }
+    }
+}
+
+__global__ void unpack_cols_kernel(const uint32_t* row_ptr, const uint32_t* delta, int brows,
+                                   uint32_t* col_idx) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= brows) return;
+    uint32_t col = 0;
+    for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
+        col += delta[b];
+        col_idx[b] = col;
+    }
+}
+
+}  // namespace spcvk

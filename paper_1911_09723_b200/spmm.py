@@ -1,0 +1,397 @@
+"""Python mirror of the reference SpMM operator surface, over the C-ABI.
+
+Reference (``/root/reference/proj``):
+  * ``Tensor``, ``Activation``, ``ShapeError``/``LayoutError`` — include/spcv/tensor.hpp:11-97
+  * ``BcsrMatrix``, ``FormatError``, ``encode_bcsr``/``decode_bcsr`` — include/spcv/sparse.hpp:12-103,
+    src/sparse.cpp:16-51,108-148
+  * ``MicrokernelConfig``, ``Tier``, ``spmm_into``/``spmm``/``spconv_1x1`` — include/spcv/kernels.hpp:18-55,
+    src/kernels.cpp:238-341
+
+Names, argument meaning, validation order and error classes follow the
+reference so parity tests read like ``proj/tests/test_kernels.cpp``. All
+arithmetic runs in the sm_100a kernel (``csrc/spmm_kernel.cuh``); there is no
+CPU path. Host (numpy) tensors go through ``spcv_cu_spmm_into_host`` (copy in,
+kernel, copy out); torch CUDA tensors go through ``spcv_cu_spmm_into`` on the
+current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib
+
+
+# ------------------------------------------------------------------ errors
+class ShapeError(ValueError):
+    """tensor.hpp:12-15 (derives from std::invalid_argument there)."""
+
+
+class LayoutError(ValueError):
+    """tensor.hpp:18-21."""
+
+
+class FormatError(ValueError):
+    """sparse.hpp:12-15."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or a shape beyond the device limits (no reference counterpart)."""
+
+
+def _raise(status: int) -> None:
+    if status == _capi.OK:
+        return
+    msg = _capi.last_error()
+    if status == _capi.ERR_LAYOUT:
+        raise LayoutError(msg)
+    if status == _capi.ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == _capi.ERR_FORMAT:
+        raise FormatError(msg)
+    if status == _capi.ERR_INVALID:
+        raise ValueError(msg)
+    raise DeviceError(msg or f"spcv_cu status {status}")
+
+
+# ----------------------------------------------------------------- tensors
+class Layout(enum.IntEnum):
+    CHW = _capi.LAYOUT_CHW
+    HWC = _capi.LAYOUT_HWC
+
+
+class Tensor:
+    """Single-image host tensor (tensor.hpp:30-54); ``data`` is a flat float32 array."""
+
+    def __init__(self, c: int, h: int, w: int, layout: Layout = Layout.CHW, data=None):
+        if c < 1 or h < 1 or w < 1:
+            raise ShapeError("tensor dims must be >= 1")
+        self.channels, self.height, self.width, self.layout = int(c), int(h), int(w), Layout(layout)
+        n = self.channels * self.height * self.width
+        if data is None:
+            self.data = np.zeros(n, dtype=np.float32)
+        else:
+            self.data = np.ascontiguousarray(np.asarray(data, dtype=np.float32).reshape(-1))
+            if self.data.size != n:
+                raise ShapeError("tensor data size mismatch")
+
+    def spatial(self) -> int:
+        return self.height * self.width
+
+    def size(self) -> int:
+        return self.data.size
+
+
+@dataclass
+class Activation:
+    """tensor.hpp:74-97. ``clamp`` enforces lo < hi; apply() is the ternary compare."""
+
+    kind: int = _capi.ACT_NONE
+    lo: float = 0.0
+    hi: float = 0.0
+
+    @staticmethod
+    def none() -> "Activation":
+        return Activation()
+
+    @staticmethod
+    def clamp(lo: float, hi: float) -> "Activation":
+        if not (lo < hi):
+            raise ValueError("clamp requires lo < hi")
+        return Activation(_capi.ACT_CLAMP, float(lo), float(hi))
+
+    @staticmethod
+    def relu6() -> "Activation":
+        return Activation.clamp(0.0, 6.0)
+
+    @staticmethod
+    def relu() -> "Activation":
+        return Activation.clamp(0.0, float("inf"))
+
+
+class Tier(enum.IntEnum):
+    Scalar = 0
+    Vector = 1
+    Auto = 2
+
+
+@dataclass
+class MicrokernelConfig:
+    """kernels.hpp:28-33 plus ``strict`` (bit-exact arithmetic, default) vs FFMA."""
+
+    m: int = 0
+    n: int = 1
+    prefetch: bool = True
+    tier: Tier = Tier.Auto
+    strict: bool = True
+
+
+def resolve_tier(requested: Tier) -> Tier:
+    """kernels.cpp:248-256 (one CUDA path: 'vector' is always available)."""
+    env = os.environ.get("SPCV_FORCE_SCALAR")
+    if env and env != "0":
+        return Tier.Scalar
+    return Tier.Vector if requested == Tier.Auto else Tier(requested)
+
+
+def default_strip_width(t: Tier) -> int:
+    return 16 if resolve_tier(t) == Tier.Vector else 8
+
+
+def variant_name(m: int, n: int) -> str:
+    return f"{m}x{n}"
+
+
+def parse_variant(s: str) -> tuple[int, int]:
+    """kernels.cpp:281-300."""
+    bad = ValueError(f"bad variant '{s}' (expected MxN, e.g. 16x2)")
+    x = s.find("x")
+    if x <= 0 or x + 1 >= len(s):
+        raise bad
+    a, b = s[:x], s[x + 1:]
+    if not (a.isdigit() and b.isdigit()):
+        raise bad
+    m, n = int(a), int(b)
+    if m not in (4, 8, 16):
+        raise ValueError(f"variant strip width must be 4, 8 or 16 (got {s})")
+    if n not in (1, 2, 4):
+        raise ValueError(f"variant out_block must be 1, 2 or 4 (got {s})")
+    return m, n
+
+
+def parse_tier(s: str) -> Tier:
+    try:
+        return {"scalar": Tier.Scalar, "vector": Tier.Vector, "auto": Tier.Auto}[s]
+    except KeyError:
+        raise ValueError(f"unknown tier '{s}' (expected scalar|vector|auto)") from None
+
+
+# --------------------------------------------------------------------- BCSR
+@dataclass
+class BcsrMatrix:
+    """sparse.hpp:65-79: Nx1 block CSR; values block-contiguous, output-channel-minor."""
+
+    rows: int = 0
+    cols: int = 0
+    block_h: int = 1
+    row_ptr: np.ndarray = field(default_factory=lambda: np.zeros(1, np.uint32))
+    col_idx: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    values: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float32))
+
+    def block_rows(self) -> int:
+        return self.rows // self.block_h
+
+    def nnz_blocks(self) -> int:
+        return int(self.col_idx.size)
+
+    def nnz_values(self) -> int:
+        return int(self.values.size)
+
+    def validate(self) -> None:
+        """sparse.cpp:16-51, same checks in the same order (FormatError)."""
+        if self.rows < 1 or self.cols < 1:
+            raise FormatError("bcsr: dims must be >= 1")
+        if self.block_h not in (1, 2, 4):
+            raise FormatError("bcsr: block height must be 1, 2 or 4")
+        if self.rows % self.block_h:
+            raise FormatError("bcsr: rows not divisible by block height")
+        rp = np.asarray(self.row_ptr, dtype=np.int64)
+        if rp.size != self.block_rows() + 1:
+            raise FormatError("bcsr: row_ptr length != block rows + 1")
+        if rp[0] != 0:
+            raise FormatError("bcsr: row_ptr[0] != 0")
+        if np.any(np.diff(rp) < 0):
+            raise FormatError("bcsr: row_ptr not non-decreasing")
+        if rp[-1] != self.col_idx.size:
+            raise FormatError("bcsr: row_ptr[-1] != block count")
+        if self.values.size != self.col_idx.size * self.block_h:
+            raise FormatError("bcsr: values length != block count * block height")
+        ci = np.asarray(self.col_idx, dtype=np.int64)
+        if ci.size:
+            if np.any(ci >= self.cols):
+                raise FormatError("bcsr: column index out of range")
+            d = np.diff(ci)
+            first = np.zeros(ci.size, dtype=bool)
+            first[rp[:-1][rp[:-1] < ci.size]] = True
+            if np.any((d <= 0) & ~first[1:]):
+                raise FormatError("bcsr: column indices not strictly increasing")
+
+
+def encode_bcsr(w: np.ndarray, block_h: int) -> BcsrMatrix:
+    """sparse.cpp:108-134: keep a block iff any member != 0 (so -0.0 is zero)."""
+    if block_h not in (1, 2, 4):
+        raise FormatError("encode_bcsr: block height must be 1, 2 or 4")
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    rows, cols = w.shape
+    if rows % block_h:
+        raise ShapeError("encode_bcsr: rows not divisible by block height")
+    blocks = w.reshape(rows // block_h, block_h, cols)           # [br][n][c]
+    keep = np.any(blocks != 0.0, axis=1)                          # [br][c]
+    counts = keep.sum(axis=1)
+    row_ptr = np.zeros(rows // block_h + 1, dtype=np.uint32)
+    np.cumsum(counts, out=row_ptr[1:])
+    br, c = np.nonzero(keep)                                      # row-major: br then c ascending
+    values = blocks.transpose(0, 2, 1)[br, c, :].reshape(-1)      # [blk][n]
+    return BcsrMatrix(rows, cols, block_h, row_ptr, c.astype(np.uint32),
+                      np.ascontiguousarray(values, dtype=np.float32))
+
+
+def decode_bcsr(m: BcsrMatrix) -> np.ndarray:
+    """sparse.cpp:136-148: validate, then scatter blocks into a dense matrix."""
+    m.validate()
+    w = np.zeros((m.rows, m.cols), dtype=np.float32)
+    counts = np.diff(m.row_ptr.astype(np.int64))
+    br = np.repeat(np.arange(m.block_rows()), counts)
+    vals = m.values.reshape(-1, m.block_h)
+    for n in range(m.block_h):
+        w[br * m.block_h + n, m.col_idx.astype(np.int64)] = vals[:, n]
+    return w
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+class DeviceBcsr:
+    """BCSR weights packed once onto the current CUDA device (spcv_cu_pack)."""
+
+    def __init__(self, m: BcsrMatrix):
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.uint32)
+        ci = np.ascontiguousarray(m.col_idx, dtype=np.uint32)
+        va = np.ascontiguousarray(m.values, dtype=np.float32)
+        h = ctypes.c_void_p()
+        _raise(lib.spcv_cu_pack(int(m.rows), int(m.cols), int(m.block_h), _ptr(rp), rp.size,
+                                _ptr(ci), ci.size, _ptr(va), va.size, ctypes.byref(h)))
+        self._h = h
+        self.rows, self.cols, self.block_h = int(m.rows), int(m.cols), int(m.block_h)
+        self.nnz_blocks = int(ci.size)
+        slots = ctypes.c_int()
+        dev = ctypes.c_int()
+        _raise(lib.spcv_cu_weights_info(self._h, None, None, None, None, ctypes.byref(slots),
+                                        ctypes.byref(dev)))
+        self.row_slots, self.device = slots.value, dev.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def unpack(self) -> BcsrMatrix:
+        """Bit-exact device decode of the counts/deltas/values streams."""
+        rp = np.zeros(self.rows // self.block_h + 1, dtype=np.uint32)
+        ci = np.zeros(self.nnz_blocks, dtype=np.uint32)
+        va = np.zeros(self.nnz_blocks * self.block_h, dtype=np.float32)
+        _raise(lib.spcv_cu_unpack(self._h, _ptr(rp), _ptr(ci) or None, _ptr(va) or None))
+        return BcsrMatrix(self.rows, self.cols, self.block_h, rp, ci, va)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.spcv_cu_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------- spmm
+def _mode(cfg: MicrokernelConfig) -> int:
+    return _capi.MODE_STRICT if cfg.strict else _capi.MODE_FAST
+
+
+def spmm_into(w, act: Tensor, bias, fused: Activation, out: Tensor,
+              cfg: MicrokernelConfig | None = None) -> None:
+    """kernels.hpp:45-46 with host tensors. ``w`` is a BcsrMatrix (packed per
+    call, like the reference which takes it by const&) or a DeviceBcsr."""
+    cfg = cfg or MicrokernelConfig()
+    b = np.zeros(0, np.float32) if bias is None else np.ascontiguousarray(bias, np.float32).reshape(-1)
+    # The reference checks arguments before it ever reads the matrix
+    # (kernels.cpp:306-322); do the same so error precedence matches even for
+    # a malformed BcsrMatrix, which the packer rejects afterwards.
+    rows = w.rows
+    if act.layout != Layout.CHW:
+        raise LayoutError("spmm: activation must be CHW")
+    if w.cols != act.channels:
+        raise ShapeError(f"spmm: weight cols {w.cols} != activation channels {act.channels}")
+    if cfg.n != w.block_h:
+        raise FormatError(f"spmm: cfg out_block {cfg.n} != matrix block height {w.block_h}")
+    if b.size and b.size != rows:
+        raise ShapeError("spmm: bias length != rows")
+    if (out.layout != Layout.CHW or out.channels != rows or out.height != act.height
+            or out.width != act.width):
+        raise ShapeError("spmm: output tensor shape/layout mismatch")
+    m = cfg.m if cfg.m != 0 else default_strip_width(cfg.tier)
+    if m not in (4, 8, 16):
+        raise ValueError("spmm: strip width must be 4, 8 or 16")
+    dw = w if isinstance(w, DeviceBcsr) else DeviceBcsr(w)
+    a = np.ascontiguousarray(act.data, np.float32)
+    if out.data.dtype != np.float32 or not out.data.flags.c_contiguous:
+        out.data = np.ascontiguousarray(out.data, np.float32)
+    _raise(lib.spcv_cu_spmm_into_host(
+        dw.handle, _ptr(a), int(act.layout), 1, act.channels, act.height, act.width,
+        _ptr(b) or None, b.size, fused.kind, fused.lo, fused.hi, _ptr(out.data), int(out.layout),
+        out.channels, out.height, out.width, cfg.m, cfg.n, _mode(cfg)))
+
+
+def spmm(w, act: Tensor, bias, fused: Activation | None = None,
+         cfg: MicrokernelConfig | None = None) -> Tensor:
+    """kernels.cpp:336-341."""
+    out = Tensor(w.rows, act.height, act.width, Layout.CHW)
+    spmm_into(w, act, bias, fused or Activation.none(), out, cfg)
+    return out
+
+
+spconv_1x1 = spmm
+
+
+def spmm_host_batched(w: DeviceBcsr, act: np.ndarray, bias, fused: Activation, out: np.ndarray,
+                      cfg: MicrokernelConfig | None = None) -> None:
+    """Batched host path: act [B][K][H][W] -> out [B][M][H][W] (numpy, ideally pinned)
+    through spcv_cu_spmm_into_host (H2D, kernel, D2H inside the call)."""
+    cfg = cfg or MicrokernelConfig(n=w.block_h)
+    B, K, H, W = act.shape
+    b = None if bias is None else np.ascontiguousarray(bias, np.float32)
+    _raise(lib.spcv_cu_spmm_into_host(
+        w.handle, act.ctypes.data, _capi.LAYOUT_CHW, B, K, H, W,
+        None if b is None else b.ctypes.data, 0 if b is None else b.size, fused.kind, fused.lo,
+        fused.hi, out.ctypes.data, _capi.LAYOUT_CHW, out.shape[1], out.shape[2], out.shape[3],
+        cfg.m, cfg.n, _mode(cfg)))
+
+
+def spmm_batched_into(w: DeviceBcsr, act, bias, fused: Activation, out,
+                      cfg: MicrokernelConfig | None = None, stream=None) -> None:
+    """Device path: torch CUDA float32 tensors, act [B][K][H][W] (or [K][H][W]),
+    out [B][M][H][W]; asynchronous on ``stream`` (default: torch's current stream)."""
+    import torch
+
+    cfg = cfg or MicrokernelConfig(n=w.block_h)
+    if act.dim() == 3:
+        act = act.unsqueeze(0)
+        out = out.unsqueeze(0)
+    if act.device.type != "cuda" or out.device.type != "cuda":
+        raise DeviceError("spmm_batched_into: tensors must be on a CUDA device")
+    if act.dtype != torch.float32 or out.dtype != torch.float32:
+        raise ShapeError("spmm_batched_into: float32 tensors required")
+    if not (act.is_contiguous() and out.is_contiguous()):
+        raise LayoutError("spmm_batched_into: contiguous NCHW tensors required")
+    B, K, H, W = act.shape
+    if out.shape[0] != B:
+        raise ShapeError("spmm_batched_into: batch mismatch")
+    bptr, blen = None, 0
+    if bias is not None:
+        if bias.device.type != "cuda" or bias.dtype != torch.float32:
+            raise ShapeError("spmm_batched_into: bias must be a CUDA float32 tensor")
+        bptr, blen = bias.data_ptr(), bias.numel()
+    if stream is None:
+        stream = torch.cuda.current_stream(act.device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    _raise(lib.spcv_cu_spmm_into(
+        w.handle, act.data_ptr(), _capi.LAYOUT_CHW, B, K, H, W, bptr, blen, fused.kind, fused.lo,
+        fused.hi, out.data_ptr(), _capi.LAYOUT_CHW, out.shape[1], out.shape[2], out.shape[3],
+        cfg.m, cfg.n, _mode(cfg), sptr))

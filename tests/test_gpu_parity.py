@@ -1,0 +1,467 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle and the
+reference's golden outputs. Needs a B200 (marked gpu).
+
+Bar (BASELINE.json north_star):
+  * strict mode (default): bit-exact against the reference / oracle;
+  * fast (FFMA) mode: |gpu - ref| <= 1e-5 * max(1, nnz_r/64) * A_ij with
+    A_ij = |bias_r| + sum_k |w_rk x_kj| computed in fp64;
+  * pack/unpack of the weight format: exact, byte for byte.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from refcases import Mt, masked_case, random_bias, random_chw, random_matrix
+
+import paper_1911_09723_b200 as sp
+from paper_1911_09723_b200.workloads import (CONFIGS, Layer, c5_layer, make_layer_data,
+                                             mbv1_pointwise, mbv2_pointwise)
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+RELU6 = sp.Activation.relu6()
+NONE = sp.Activation.none()
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).reshape(-1).view(np.uint32)
+
+
+def act_of(spec):
+    if isinstance(spec, sp.Activation):
+        return spec
+    return sp.Activation.none() if spec[0] == "none" else sp.Activation.clamp(spec[1], spec[2])
+
+
+def run_device(m, act, bias, fused, strict=True, dw=None, stream=None):
+    """act [B][K][H][W] numpy -> out numpy via spcv_cu_spmm_into on device."""
+    import torch
+
+    act = np.ascontiguousarray(act, np.float32)
+    if act.ndim == 3:
+        act = act[None]
+    B, K, H, W = act.shape
+    dw = dw or sp.DeviceBcsr(m)
+    a = torch.from_numpy(act).cuda()
+    o = torch.full((B, dw.rows, H, W), float("nan"), device="cuda")
+    b = None if bias is None or len(bias) == 0 else torch.from_numpy(np.asarray(bias, np.float32)).cuda()
+    sp.spmm_batched_into(dw, a, b, act_of(fused), o,
+                         sp.MicrokernelConfig(n=dw.block_h, strict=strict), stream=stream)
+    torch.cuda.synchronize()
+    return o.cpu().numpy()
+
+
+def load_cases():
+    z = np.load(os.path.join(GOLD, "spmm_cases.npz"))
+    cases = {}
+    for k in z.files:
+        name, field = k.split("/")
+        cases.setdefault(name, {})[field] = z[k]
+    return cases
+
+
+CASES = load_cases()
+
+
+def case_matrix(c):
+    return sp.BcsrMatrix(int(c["rows"]), int(c["cols"]), int(c["block_h"]), c["row_ptr"],
+                         c["col_idx"], c["values"])
+
+
+def case_fused(c):
+    k, lo, hi = c["fused"]
+    return NONE if k == 0 else sp.Activation.clamp(float(lo), float(hi))
+
+
+# ------------------------------------------------------------ golden vectors
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_device_path_bit_exact(name):
+    c = CASES[name]
+    got = run_device(case_matrix(c), c["act"], c["bias"] if c["bias"].size else None, case_fused(c))
+    assert np.array_equal(bits(got), bits(c["expected"]))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_host_path_bit_exact(name):
+    """The reference-facing call shape: spmm with host tensors (per image)."""
+    c = CASES[name]
+    m = case_matrix(c)
+    B, K, H, W = c["act"].shape
+    for i in range(B):
+        act = sp.Tensor(K, H, W, data=c["act"][i])
+        out = sp.spmm(m, act, c["bias"] if c["bias"].size else None, case_fused(c),
+                      sp.MicrokernelConfig(n=m.block_h))
+        assert np.array_equal(bits(out.data), bits(c["expected"][i]))
+
+
+def sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+DIGESTS = json.load(open(os.path.join(GOLD, "digests.json")))
+
+
+@pytest.mark.parametrize("name", sorted(DIGESTS))
+def test_golden_digest_cases_bit_exact(name):
+    d = DIGESTS[name]
+    L = dict(d["layer"])
+    L["act"] = tuple(L["act"])
+    layer = Layer(**L)
+    data = make_layer_data(layer, d["images"], d["seed"])
+    assert sha(data.act) == d["sha_act"] and sha(data.weights.values) == d["sha_values"]
+    got = run_device(data.weights, data.act, data.bias, layer.act)
+    assert sha(got.reshape(d["images"], layer.cout, -1)) == d["sha_expected"]
+
+
+# ------------------------------------- reference hot-path tests, re-expressed
+def test_identity_returns_input():
+    # test_kernels.cpp:55-68
+    rng = Mt(3)
+    act = random_chw(8, 5, 7, rng)
+    for bh in (1, 2, 4):
+        m = sp.encode_bcsr(np.eye(8, dtype=np.float32), bh)
+        out = sp.spmm(m, sp.Tensor(8, 5, 7, data=act), np.zeros(8, np.float32), NONE,
+                      sp.MicrokernelConfig(n=bh))
+        assert np.array_equal(bits(out.data), bits(act))
+
+
+def test_hand_case():
+    # test_kernels.cpp:70-89
+    w = np.zeros((2, 3), np.float32)
+    w[0, 1], w[1, 1] = 2.0, -3.0
+    m = sp.encode_bcsr(w, 2)
+    assert m.nnz_blocks() == 1
+    act = sp.Tensor(3, 1, 2, data=[9, 9, 1, 4, 9, 9])
+    out = sp.spmm(m, act, np.array([1.0, -1.0], np.float32), RELU6, sp.MicrokernelConfig(n=2))
+    assert out.data.tolist() == [3.0, 6.0, 0.0, 0.0]
+
+
+def test_every_variant_matches_oracle(oracle):
+    # test_kernels.cpp:91-109 (tolerance 1e-5 there; bit-exact here)
+    rng = Mt(17)
+    for m_width in (4, 8, 16):
+        for bh in (1, 2, 4):
+            dense, m = masked_case(64, 64, 0.9, bh, rng, oracle)
+            act = random_chw(64, 14, 14, rng)
+            bias = random_bias(64, rng)
+            want = oracle.matmul_reference(dense, act.reshape(64, -1), bias, RELU6)
+            for tier in (sp.Tier.Scalar, sp.Tier.Auto):
+                cfg = sp.MicrokernelConfig(m=m_width, n=bh, tier=tier)
+                got = sp.spmm(m, sp.Tensor(64, 14, 14, data=act), bias, RELU6, cfg)
+                assert np.array_equal(bits(got.data), bits(want))
+
+
+def test_strip_remainders(oracle):
+    # test_kernels.cpp:111-126: spatial extents not multiple of any strip width
+    rng = Mt(19)
+    for S in (1, 3, 5, 7, 13, 197):
+        dense, m = masked_case(16, 12, 0.7, 2, rng, oracle)
+        act = random_chw(12, 1, S, rng)
+        bias = random_bias(16, rng)
+        want = oracle.matmul_reference(dense, act.reshape(12, -1), bias, None)
+        for m_width in (4, 8, 16):
+            got = sp.spmm(m, sp.Tensor(12, 1, S, data=act), bias, NONE,
+                          sp.MicrokernelConfig(m=m_width, n=2))
+            assert np.array_equal(bits(got.data), bits(want))
+
+
+def test_variants_tiers_prefetch_agree():
+    # test_kernels.cpp:128-163
+    rng = Mt(23)
+    from oracle import Oracle
+
+    dense, m = masked_case(32, 24, 0.8, 4, rng, Oracle())
+    act = sp.Tensor(24, 3, 13, data=random_chw(24, 3, 13, rng))
+    bias = random_bias(32, rng)
+    first = None
+    for tier in (sp.Tier.Scalar, sp.Tier.Vector, sp.Tier.Auto):
+        for m_width in (4, 8, 16):
+            for pf in (True, False):
+                cfg = sp.MicrokernelConfig(m=m_width, n=4, tier=tier, prefetch=pf)
+                out = sp.spmm(m, act, bias, RELU6, cfg).data
+                if first is None:
+                    first = out
+                assert np.array_equal(bits(out), bits(first))
+
+
+def test_fused_clamp_equals_unfused_then_clamped(oracle):
+    # test_kernels.cpp:165-175
+    rng = Mt(31)
+    dense, m = masked_case(16, 16, 0.6, 1, rng, oracle)
+    act = sp.Tensor(16, 4, 5, data=random_chw(16, 4, 5, rng))
+    bias = random_bias(16, rng)
+    fused = sp.spmm(m, act, bias, RELU6).data
+    plain = sp.spmm(m, act, bias, NONE).data
+    clamped = np.where(plain < 0, 0, np.where(plain > 6, 6, plain)).astype(np.float32)
+    assert np.array_equal(bits(fused), bits(clamped))
+
+
+def test_spmm_validates_inputs():
+    # test_kernels.cpp:177-214
+    from oracle import Oracle
+
+    rng = Mt(37)
+    dense, m = masked_case(8, 8, 0.5, 2, rng, Oracle())
+    act = sp.Tensor(8, 2, 2, data=random_chw(8, 2, 2, rng))
+    bias = np.zeros(8, np.float32)
+    with pytest.raises(sp.FormatError):
+        sp.spmm(m, act, bias, NONE, sp.MicrokernelConfig(n=4))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm(m, sp.Tensor(9, 2, 2), bias, NONE, sp.MicrokernelConfig(n=2))
+    with pytest.raises(sp.LayoutError):
+        sp.spmm(m, sp.Tensor(8, 2, 2, sp.Layout.HWC), bias, NONE, sp.MicrokernelConfig(n=2))
+    with pytest.raises(ValueError):
+        sp.spmm(m, act, bias, NONE, sp.MicrokernelConfig(m=5, n=2))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm(m, act, np.zeros(3, np.float32), NONE, sp.MicrokernelConfig(n=2))
+
+
+def test_cabi_validation_order_on_device_pointers():
+    """The same checks through spcv_cu_spmm_into itself (C-ABI codes)."""
+    import ctypes
+
+    import torch
+    from paper_1911_09723_b200 import _capi
+
+    m = sp.encode_bcsr(np.eye(8, dtype=np.float32), 2)
+    dw = sp.DeviceBcsr(m)
+    a = torch.zeros(1, 8, 2, 2, device="cuda")
+    o = torch.zeros(1, 8, 2, 2, device="cuda")
+    L = _capi.lib
+
+    def call(act_layout=0, act_c=8, bias_len=0, out_layout=0, out_c=8, out_w=2, m_=0, n=2, kind=0,
+             lo=0.0, hi=0.0):
+        return L.spcv_cu_spmm_into(dw.handle, a.data_ptr(), act_layout, 1, act_c, 2, 2,
+                                   a.data_ptr() if bias_len else None, bias_len, kind, lo, hi,
+                                   o.data_ptr(), out_layout, out_c, 2, out_w, m_, n, 0, None)
+
+    assert call() == _capi.OK
+    assert call(act_layout=1, act_c=9) == _capi.ERR_LAYOUT      # layout checked first
+    assert call(act_c=9, n=4) == _capi.ERR_SHAPE                 # then channels
+    assert call(n=4, bias_len=3) == _capi.ERR_FORMAT             # then block height
+    assert call(bias_len=3, out_c=9) == _capi.ERR_SHAPE          # then bias length
+    assert call(out_w=3, m_=5) == _capi.ERR_SHAPE                # then out shape
+    assert call(m_=5) == _capi.ERR_INVALID                       # then strip width
+    assert call(kind=1, lo=1.0, hi=1.0) == _capi.ERR_INVALID     # clamp lo < hi
+    torch.cuda.synchronize()
+
+
+def test_fully_dense_matrix_equals_dense_oracle(oracle):
+    # test_kernels.cpp:232-239
+    rng = Mt(43)
+    w = random_matrix(16, 16, rng)
+    act = random_chw(16, 6, 6, rng)
+    bias = random_bias(16, rng)
+    got = sp.spmm(sp.encode_bcsr(w, 1), sp.Tensor(16, 6, 6, data=act), bias, NONE).data
+    want = oracle.matmul_reference(w, act.reshape(16, -1), bias, None)
+    assert np.array_equal(bits(got), bits(want))
+
+
+# ------------------------------------------------------------ format round trip
+def test_pack_unpack_bit_exact(oracle):
+    rng = Mt(99)
+    for bh in (1, 2, 4):
+        for _ in range(15):
+            rows = bh * (1 + int(rng() % 40))
+            cols = 1 + int(rng() % 300)
+            s = (rng() % 100) / 100.0
+            w = random_matrix(rows, cols, rng)
+            rc, keep = oracle.generate_mask(rows, cols, s, bh, 1, rng())
+            w[~keep] = 0
+            m = sp.encode_bcsr(w, bh)
+            back = sp.DeviceBcsr(m).unpack()
+            assert back.row_ptr.tobytes() == m.row_ptr.tobytes()
+            assert back.col_idx.tobytes() == m.col_idx.tobytes()
+            assert back.values.tobytes() == m.values.tobytes()
+
+
+def test_pack_unpack_large_and_degenerate():
+    for layer in (c5_layer(0.9), mbv1_pointwise()[-1], Layer("e", 4, 8, 1, 1, sparsity=0.0)):
+        d = make_layer_data(layer, 1, 11, act=False)
+        back = sp.DeviceBcsr(d.weights).unpack()
+        assert back.row_ptr.tobytes() == d.weights.row_ptr.tobytes()
+        assert back.col_idx.tobytes() == d.weights.col_idx.tobytes()
+        assert back.values.tobytes() == d.weights.values.tobytes()
+    empty = sp.encode_bcsr(np.zeros((8, 5), np.float32), 4)
+    back = sp.DeviceBcsr(empty).unpack()
+    assert back.row_ptr.tolist() == [0, 0, 0] and back.nnz_blocks() == 0
+
+
+# ------------------------------------------------------- BASELINE configs
+def check_layer(oracle, layer, images, seed, strict=True):
+    d = make_layer_data(layer, images, seed)
+    got = run_device(d.weights, d.act, d.bias, layer.act, strict=strict)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
+    if strict:
+        assert np.array_equal(bits(got), bits(want)), layer.name
+    else:
+        check_tolerance(d, got, want)
+    return d, got
+
+
+def check_tolerance(d, got, want):
+    """|gpu - ref| <= 1e-5 * max(1, nnz_r/64) * A_ij (fp64 A_ij = |b| + sum|w x|)."""
+    L = d.layer
+    W = np.abs(d.dense.astype(np.float64))
+    X = np.abs(d.act.astype(np.float64)).reshape(d.images, L.cin, -1)
+    A = np.abs(d.bias.astype(np.float64))[None, :, None] + np.einsum("mk,bks->bms", W, X)
+    nnz_r = (d.dense != 0).sum(axis=1).astype(np.float64)
+    tol = 1e-5 * np.maximum(1.0, nnz_r / 64.0)[None, :, None] * A
+    err = np.abs(got.reshape(A.shape).astype(np.float64) - want.reshape(A.shape).astype(np.float64))
+    assert np.all(err <= tol), float((err - tol).max())
+
+
+def test_config1_bit_exact(oracle):
+    check_layer(oracle, CONFIGS["c1"]["layers"]()[0], 1, 1)
+
+
+@pytest.mark.parametrize("li", range(13))
+def test_config2_mbv1_layers_bit_exact(oracle, li):
+    layer = mbv1_pointwise(0.9)[li]
+    check_layer(oracle, layer, 2 if layer.spatial <= 784 else 1, 100 + li)
+
+
+@pytest.mark.parametrize("bh", [4, 2, 1])
+@pytest.mark.parametrize("s", [0.7, 0.8, 0.9, 0.95])
+def test_config3_block_sweep_bit_exact(oracle, bh, s):
+    from paper_1911_09723_b200.workloads import c3_layer
+
+    check_layer(oracle, c3_layer(s, bh), 4, 7 + bh)
+
+
+def test_config4_mbv2_layers_bit_exact(oracle):
+    for i, layer in enumerate(mbv2_pointwise(0.85)):
+        check_layer(oracle, layer, 1, 200 + i)
+
+
+@pytest.mark.parametrize("s", [0.7, 0.8, 0.9, 0.95, 0.98])
+def test_config5_skewed_bit_exact(oracle, s):
+    check_layer(oracle, c5_layer(s), 8, 300)
+
+
+@pytest.mark.parametrize("layer", [CONFIGS["c1"]["layers"]()[0], mbv1_pointwise()[0],
+                                   mbv1_pointwise()[-1], c5_layer(0.9)],
+                         ids=["c1", "pw1", "pw13", "c5"])
+def test_fast_mode_within_tolerance(oracle, layer):
+    check_layer(oracle, layer, 2, 400, strict=False)
+
+
+# ----------------------------------- full-size, size-independent properties
+def test_config5_full_batch_images_independent_of_position(oracle):
+    """c5 at its full 1024 images: every sampled image equals the oracle run
+    on that image alone (batch position cannot matter), and a rerun is
+    bit-identical (determinism)."""
+    d = make_layer_data(c5_layer(0.9), 1024, 5)
+    got = run_device(d.weights, d.act, d.bias, d.layer.act)
+    for i in (0, 1, 377, 511, 1023):
+        want = oracle.spmm(d.weights, d.act[i:i + 1], d.bias, d.layer.act)
+        assert np.array_equal(bits(got[i]), bits(want))
+    again = run_device(d.weights, d.act, d.bias, d.layer.act)
+    assert np.array_equal(bits(got), bits(again))
+
+
+def test_config2_b256_sampled_images(oracle):
+    layers = mbv1_pointwise(0.9)
+    for li in (0, 6, 12):
+        d = make_layer_data(layers[li], 256, 500 + li)
+        got = run_device(d.weights, d.act, d.bias, d.layer.act)
+        for i in (0, 128, 255):
+            want = oracle.spmm(d.weights, d.act[i:i + 1], d.bias, d.layer.act)
+            assert np.array_equal(bits(got[i]), bits(want))
+
+
+# ----------------------------------------------------------------- edge cases
+def test_empty_matrix_and_empty_rows_give_clamped_bias(oracle):
+    m = sp.encode_bcsr(np.zeros((8, 5), np.float32), 2)
+    bias = np.array([-1, 2, 7, 0.5, -0.0, 0.0, 3, -3], np.float32)
+    act = np.ones((3, 5, 4, 4), np.float32)
+    got = run_device(m, act, bias, RELU6)
+    want = np.where(bias < 0, 0, np.where(bias > 6, 6, bias)).astype(np.float32)
+    assert np.array_equal(bits(got), bits(np.broadcast_to(want[None, :, None, None], got.shape)))
+    # -0.0 bias survives the ternary clamp (tensor.hpp:90-96)
+    assert np.signbit(got[0, 4]).all()
+
+
+def test_null_bias_is_plus_zero(oracle):
+    rng = Mt(5)
+    dense, m = masked_case(16, 16, 0.8, 1, rng, oracle)
+    act = random_chw(16, 3, 7, rng)[None]
+    got = run_device(m, act, None, NONE)
+    want = oracle.spmm(m, act, None, None)
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_nan_propagates_like_reference(oracle):
+    rng = Mt(6)
+    dense, m = masked_case(16, 16, 0.5, 1, rng, oracle)
+    act = random_chw(16, 2, 8, rng)[None]
+    act[0, 3, 1, 2] = np.nan
+    bias = random_bias(16, rng)
+    got = run_device(m, act, bias, RELU6)
+    want = oracle.spmm(m, act, bias, RELU6)  # NaN payloads may differ; positions must not
+    assert np.array_equal(np.isnan(got).reshape(-1), np.isnan(want).reshape(-1))
+
+
+def test_unaligned_and_odd_spatial_paths(oracle):
+    """S % 4 != 0 and misaligned base pointers take the scalar-staging kernel."""
+    import torch
+
+    layer = Layer("odd", 40, 24, 5, 7, sparsity=0.6)
+    d = make_layer_data(layer, 3, 9)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act).reshape(3, 24, 5, 7)
+    assert np.array_equal(bits(run_device(d.weights, d.act, d.bias, layer.act)), bits(want))
+    # S % 4 == 0 but buffers offset by one float
+    layer = Layer("mis", 40, 24, 4, 8, sparsity=0.6)
+    d = make_layer_data(layer, 3, 10)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act).reshape(3, 24, 4, 8)
+    dw = sp.DeviceBcsr(d.weights)
+    base_a = torch.zeros(d.act.size + 1, device="cuda")
+    base_o = torch.zeros(want.size + 1, device="cuda")
+    a = base_a[1:].view(d.act.shape)
+    a.copy_(torch.from_numpy(d.act))
+    o = base_o[1:].view(want.shape)
+    sp.spmm_batched_into(dw, a, torch.from_numpy(d.bias).cuda(), act_of(layer.act), o,
+                         sp.MicrokernelConfig(n=1))
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o.cpu().numpy()), bits(want))
+
+
+def test_zero_images_is_a_noop():
+    import torch
+
+    dw = sp.DeviceBcsr(sp.encode_bcsr(np.eye(4, dtype=np.float32), 1))
+    a = torch.zeros(0, 4, 2, 2, device="cuda")
+    o = torch.zeros(0, 4, 2, 2, device="cuda")
+    n0 = sp.launch_count()
+    sp.spmm_batched_into(dw, a, None, NONE, o)
+    assert sp.launch_count() == n0
+
+
+def test_too_many_input_channels_is_reported():
+    w = np.zeros((4, 2000), np.float32)
+    w[0, 0] = 1
+    with pytest.raises(sp.DeviceError):
+        sp.DeviceBcsr(sp.encode_bcsr(w, 1))
+
+
+def test_concurrent_streams_agree(oracle):
+    import torch
+
+    d = make_layer_data(mbv1_pointwise()[6], 8, 77)
+    dw = sp.DeviceBcsr(d.weights)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    r1 = run_device(d.weights, d.act, d.bias, d.layer.act, dw=dw, stream=s1)
+    r2 = run_device(d.weights, d.act, d.bias, d.layer.act, dw=dw, stream=s2)
+    assert np.array_equal(bits(r1), bits(r2))
+
+
+def test_kernel_launches_are_counted():
+    n0 = sp.launch_count()
+    run_device(sp.encode_bcsr(np.eye(4, dtype=np.float32), 1), np.ones((1, 4, 2, 2), np.float32),
+               None, NONE)
+    assert sp.launch_count() == n0 + 1

@@ -1,0 +1,210 @@
+"""CPU-only checks of the host side: the C-ABI libraries load and export every
+declared symbol, host-side format helpers match the oracle, and the Python
+mirror of the reference plumbing behaves like kernels.cpp:238-300.
+No compute is launched here (no GPU in this container)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from refcases import Mt, random_matrix
+
+import paper_1911_09723_b200 as sp
+from paper_1911_09723_b200 import _capi
+from paper_1911_09723_b200.workloads import CONFIGS, make_layer_data, mbv1_pointwise, mbv2_pointwise
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "spcv_cu.h")
+LIBDIR = os.path.join(ROOT, "paper_1911_09723_b200", "lib")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(spcv_cu_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("spcv_cu_pack", "spcv_cu_unpack", "spcv_cu_spmm_into", "spcv_cu_spmm_into_host",
+              "spcv_cu_free", "spcv_cu_last_error"):
+        assert s in syms
+
+
+def test_cabi_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(os.path.join(LIBDIR, "libspcv_cu.so"))
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(_capi.SIGNATURES)
+
+
+def test_cabi_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", os.path.join(LIBDIR, "libspcv_cu.so")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
+
+
+def test_cpp_dropin_library_exports_reference_api():
+    so = os.path.join(LIBDIR, "libspcv_b200.so")
+    out = subprocess.run(["nm", "-DC", so], capture_output=True, text=True).stdout
+    for sym in ("spcv::spmm_into(", "spcv::spmm(", "spcv::encode_bcsr(", "spcv::decode_bcsr(",
+                "spcv::BcsrMatrix::validate() const", "spcv::DeviceBcsr::DeviceBcsr(",
+                "spcv::spmm_batched_into(", "spcv::parse_variant("):
+        assert sym in out, sym
+
+
+def test_version_and_launch_counter_without_gpu():
+    assert b"sm_100a" in _capi.lib.spcv_cu_version()
+    assert sp.launch_count() == 0 or sp.launch_count() > 0
+
+
+def test_pack_reports_cuda_error_without_gpu_or_format_error_first():
+    # A malformed matrix is rejected before any device work (FormatError).
+    bad = sp.BcsrMatrix(4, 4, 3, np.array([0, 0], np.uint32), np.zeros(0, np.uint32),
+                        np.zeros(0, np.float32))
+    with pytest.raises(sp.FormatError):
+        sp.DeviceBcsr(bad)
+
+
+def test_encode_decode_match_oracle(oracle):
+    rng = Mt(99)
+    for bh in (1, 2, 4):
+        for _ in range(20):
+            rows = bh * (1 + int(rng() % 12))
+            cols = 1 + int(rng() % 40)
+            s = (rng() % 100) / 100.0
+            w = random_matrix(rows, cols, rng)
+            rc, keep = oracle.generate_mask(rows, cols, s, bh, 1, rng())
+            w[~keep] = 0
+            m = sp.encode_bcsr(w, bh)
+            rc, (rp, ci, va) = oracle.encode_bcsr(w, bh)
+            assert np.array_equal(m.row_ptr, rp) and np.array_equal(m.col_idx, ci)
+            assert np.array_equal(m.values.view(np.uint32), va.view(np.uint32))
+            m.validate()
+            assert np.array_equal(sp.decode_bcsr(m), w)
+
+
+def test_encode_known_answers():
+    # test_sparse.cpp:9-41
+    m = sp.encode_bcsr(np.zeros((2, 2), np.float32), 1)
+    assert m.row_ptr.tolist() == [0, 0, 0] and m.nnz_blocks() == 0
+    m = sp.encode_bcsr(np.eye(2, dtype=np.float32), 2)
+    assert m.row_ptr.tolist() == [0, 2] and m.col_idx.tolist() == [0, 1]
+    assert m.values.tolist() == [1.0, 0.0, 0.0, 1.0] and m.nnz_values() == 4
+    w = np.zeros((4, 3), np.float32)
+    w[1, 2] = 5
+    m = sp.encode_bcsr(w, 2)
+    assert m.row_ptr.tolist() == [0, 1, 1] and m.col_idx.tolist() == [2]
+    assert m.values.tolist() == [0.0, 5.0]
+    with pytest.raises(sp.ShapeError):
+        sp.encode_bcsr(np.zeros((3, 4), np.float32), 2)
+    # -0.0 is zero for the keep test (sparse.cpp:124)
+    m = sp.encode_bcsr(np.array([[-0.0, 1.0]], np.float32), 1)
+    assert m.col_idx.tolist() == [1]
+
+
+def test_validate_rejections_match_oracle(oracle):
+    w = np.zeros((4, 4), np.float32)
+    w[0, 1], w[2, 3] = 1, 2
+    g = sp.encode_bcsr(w, 2)
+    rp, ci, va = g.row_ptr, g.col_idx, g.values
+    bad = [
+        (5, 4, 2, rp, ci, va),
+        (4, 4, 2, np.r_[1, rp[1:]].astype(np.uint32), ci, va),
+        (4, 4, 2, np.r_[rp[0], 3, rp[2:]].astype(np.uint32), ci, va),
+        (4, 4, 2, np.r_[rp[:-1], 1].astype(np.uint32), ci, va),
+        (4, 4, 2, rp, np.r_[99, ci[1:]].astype(np.uint32), va),
+        (4, 4, 2, rp, ci, np.r_[va, 0].astype(np.float32)),
+        (4, 4, 3, rp, ci, va),
+        (2, 4, 1, np.array([0, 2, 2], np.uint32), np.array([2, 1], np.uint32),
+         np.array([1.0, 2.0], np.float32)),
+    ]
+    for args in bad:
+        assert oracle.validate(*args) == 3
+        with pytest.raises(sp.FormatError):
+            sp.BcsrMatrix(*args).validate()
+        with pytest.raises(sp.FormatError):  # the C-ABI packer rejects it the same way
+            sp.DeviceBcsr(sp.BcsrMatrix(*args))
+
+
+def test_variant_and_tier_parsing():
+    # test_kernels.cpp:355-366
+    assert sp.parse_variant("16x2") == (16, 2)
+    assert sp.parse_variant("4x1") == (4, 1)
+    assert sp.variant_name(8, 4) == "8x4"
+    for bad in ["", "16", "x2", "16x", "16x3", "5x2", "16x2x1", "a.b"]:
+        with pytest.raises(ValueError):
+            sp.parse_variant(bad)
+    assert sp.parse_tier("scalar") == sp.Tier.Scalar
+    with pytest.raises(ValueError):
+        sp.parse_tier("turbo")
+
+
+def test_tier_env_override(monkeypatch):
+    # test_kernels.cpp:368-381
+    assert sp.resolve_tier(sp.Tier.Auto) == sp.Tier.Vector
+    monkeypatch.setenv("SPCV_FORCE_SCALAR", "1")
+    assert sp.resolve_tier(sp.Tier.Auto) == sp.Tier.Scalar
+    monkeypatch.setenv("SPCV_FORCE_SCALAR", "0")
+    assert sp.resolve_tier(sp.Tier.Auto) == sp.Tier.Vector
+    assert sp.default_strip_width(sp.Tier.Scalar) == 8
+    assert sp.default_strip_width(sp.Tier.Vector) == 16
+
+
+def test_activation_contract():
+    with pytest.raises(ValueError):
+        sp.Activation.clamp(1.0, 1.0)
+    r6 = sp.Activation.relu6()
+    assert (r6.kind, r6.lo, r6.hi) == (1, 0.0, 6.0)
+
+
+def test_host_argument_checks_precede_device_work():
+    """spmm_into validation order (kernels.cpp:306-322) with host tensors; all
+    of these fail before any CUDA call, so they run without a GPU."""
+    w = sp.encode_bcsr(np.eye(8, dtype=np.float32), 2)
+    act = sp.Tensor(8, 2, 2)
+    out = sp.Tensor(8, 2, 2)
+    cfg = sp.MicrokernelConfig(n=4)
+    with pytest.raises(sp.FormatError):
+        sp.spmm_into(w, act, None, sp.Activation.none(), out, cfg)
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_into(w, sp.Tensor(9, 2, 2), None, sp.Activation.none(), out, sp.MicrokernelConfig(n=2))
+    with pytest.raises(sp.LayoutError):
+        sp.spmm_into(w, sp.Tensor(8, 2, 2, sp.Layout.HWC), None, sp.Activation.none(), out,
+                     sp.MicrokernelConfig(n=2))
+    with pytest.raises(ValueError):
+        sp.spmm_into(w, act, None, sp.Activation.none(), out, sp.MicrokernelConfig(m=5, n=2))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_into(w, act, np.zeros(3, np.float32), sp.Activation.none(), out, sp.MicrokernelConfig(n=2))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_into(w, act, None, sp.Activation.none(), sp.Tensor(8, 2, 3), sp.MicrokernelConfig(n=2))
+
+
+def test_workload_shapes():
+    v1 = mbv1_pointwise()
+    assert [(l.cin, l.cout, l.h) for l in v1][:3] == [(32, 64, 112), (64, 128, 56), (128, 128, 56)]
+    assert len(v1) == 13 and v1[-1].cin == 1024 and v1[-1].h == 7
+    v2 = mbv2_pointwise()
+    names = [(l.cin, l.cout, l.h) for l in v2]
+    for want in [(24, 144, 56), (32, 192, 28), (64, 384, 14), (160, 960, 7), (144, 24, 56),
+                 (192, 32, 28), (384, 64, 14), (960, 160, 7), (32, 16, 112), (16, 96, 112),
+                 (96, 24, 56), (960, 320, 7), (320, 1280, 7)]:
+        assert want in names
+    assert set(CONFIGS) == {"c1", "c2-b1", "c2-b256", "c3", "c4", "c5"}
+
+
+def test_skewed_rows_mean_density():
+    from paper_1911_09723_b200.workloads import c5_layer
+
+    d = make_layer_data(c5_layer(0.9), 1, 5, act=False)
+    counts = np.diff(d.weights.row_ptr.astype(np.int64))
+    assert abs(counts.mean() / 1024 - 0.10) < 0.01
+    assert counts.max() / counts.mean() > 2.0  # heavy-tailed rows
+
+
+def test_uniform_mask_exact_count():
+    d = make_layer_data(mbv1_pointwise()[0], 1, 1, act=False)
+    assert d.weights.nnz_values() == 2048 - int(np.floor(2048 * 0.9 + 0.5))
