@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 sparse 1x1-conv SpMM (the north-star path).
+
+Default workload (BASELINE.json configs[1]): the 13 MobileNet-v1-1.0 pointwise
+layers at 224x224, 90% unstructured sparsity, ReLU6, fp32, 256 images per GPU
+(weak scaling: each rank runs its own 256-image shard, no collective on the
+data path). One step = one pass of all 13 layers over the rank's batch.
+
+Metric (BASELINE.json): effective GFLOP/s = 2*nnz*N / t summed over layers
+(reference convention, /root/reference/proj/src/bench.cpp:211), plus
+algorithmic HBM GB/s against the measured peak.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line on stdout; details go to stderr.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1911_09723_b200.workloads import CONFIGS, activation_of, make_layer_data  # noqa: E402
+
+WORKLOAD_DESC = {
+    "c2-b256": "MobileNet-v1-1.0 pointwise stack @224 (13 layers), 90% unstructured, ReLU6",
+    "c2-b1": "MobileNet-v1-1.0 pointwise stack @224 (13 layers), 90% unstructured, ReLU6",
+    "c1": "single 128x128 sparse 1x1 conv @28x28, 80% unstructured, ReLU",
+    "c3": "512x512 @14x14, block 4/2/1 x1, sparsity 70-95%, ReLU",
+    "c4": "MobileNet-v2-1.0 1x1 convs @224, 85% unstructured, ReLU6/linear",
+    "c5": "1024x1024 @7x7, Beta(2,8)-skewed rows, sparsity 70-98%, ReLU",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- dist glue
+class Dist:
+    def __init__(self, backend):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self, device=None):
+        if self.pg:
+            if device is not None:
+                self.pg.barrier(device_ids=[device])
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float, device=None) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device=device or "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ------------------------------------------------------------- clock probe
+class ClockProbe:
+    """Samples SM clock and throttle reasons via NVML every 10 ms while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - box-specific
+            log(f"clock probe unavailable: {e}")
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"], "samples": 0}
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU reference
+def cpu_reference_run(layers_data, steps: int, warmup: int, threads: int):
+    """Reference spmm_into (oracle/_ref, else the oracle port) on host cores.
+    Every (layer, image) pair is one spmm_into call; `threads` host threads
+    pull them longest-first (oracle/ref_shim.cpp: ref_bench_layers)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc  # CPU baseline leg only
+
+    flops = sum(d.flops() for d in layers_data)
+    if orc.have_ref():
+        ref = orc.Ref()
+        times = ref.bench_layers([(d.weights, d.act, d.bias, d.layer.act) for d in layers_data],
+                                 threads, warmup, steps)
+        return "reference", flops, times
+    port = orc.Oracle()
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        for d in layers_data:
+            port.spmm(d.weights, d.act, d.bias, d.layer.act, nthreads=threads)
+        if s >= warmup:
+            times.append(time.perf_counter() - t0)
+    return "port", flops, times
+
+
+# ------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", default="c2-b256", choices=sorted(CONFIGS))
+    ap.add_argument("--images", type=int, default=None, help="images per GPU (default: config's)")
+    ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-images", type=int, default=None, help="CPU baseline sample, images")
+    ap.add_argument("--layers-json", default=None, help="write per-layer results here")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup < 3 is not allowed by the timing rules; using 3")
+        args.warmup = 3
+
+    cfg = CONFIGS[args.config]
+    layers = cfg["layers"]()
+    images = args.images or cfg["images"]
+    hbm_peak, peak_kind = peaks()
+
+    if args.impl == "reference":
+        return run_reference(args, layers, images)
+
+    import torch
+
+    dist = Dist("nccl")
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    import paper_1911_09723_b200 as sp
+
+    # ---- data: weights identical on every rank, activations per-rank shard
+    t0 = time.time()
+    data = []
+    for li, L in enumerate(layers):
+        d = make_layer_data(L, images, 1000 * (li + 1) + dist.rank)
+        w = make_layer_data(L, 1, 1000 * (li + 1), act=False)  # weights: rank-independent seed
+        d.weights, d.dense, d.bias = w.weights, w.dense, w.bias
+        data.append(d)
+    log(f"[rank {dist.rank}] generated {len(layers)} layers x {images} images in {time.time() - t0:.1f}s")
+
+    stream = torch.cuda.Stream(dev)
+    mode_cfg = {}
+    dev_layers = []
+    for d in data:
+        dw = sp.DeviceBcsr(d.weights)
+        a = torch.from_numpy(d.act).to(dev)
+        o = torch.empty((images, d.layer.cout, d.layer.h, d.layer.w), device=dev)
+        b = torch.from_numpy(d.bias).to(dev)
+        cfgk = sp.MicrokernelConfig(n=d.layer.block_h, strict=(args.mode == "strict"))
+        dev_layers.append((dw, a, b, o, activation_of(d.layer.act), cfgk))
+        mode_cfg[d.layer.name] = dw.row_slots
+    torch.cuda.synchronize()
+
+    def step(evs=None):
+        for li, (dw, a, b, o, fused, cfgk) in enumerate(dev_layers):
+            if evs is not None:
+                evs[li][0].record(stream)
+            sp.spmm_batched_into(dw, a, b, fused, o, cfgk, stream=stream)
+            if evs is not None:
+                evs[li][1].record(stream)
+
+    flops_step = sum(d.flops() for d in data)
+    bytes_step = sum(d.alg_bytes() for d in data)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        nl = len(dev_layers)
+        lev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
+               for _ in range(args.steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier(dev)
+        torch.cuda.synchronize()
+        launches0 = sp.launch_count()
+        with ClockProbe(dev) as clk:
+            start.record(stream)
+            for k in range(args.steps):
+                step(lev[k])
+            end.record(stream)
+            torch.cuda.synchronize()
+        launches = sp.launch_count() - launches0
+        dist.barrier(dev)
+    ms_local = start.elapsed_time(end)
+    ms_total = dist.max(ms_local, device=torch.device("cuda", dev))
+    ms_step = ms_total / args.steps
+
+    # per-layer kernel times (events on the launch stream, averaged over steps)
+    per_layer = []
+    for li, d in enumerate(data):
+        us = statistics.mean(lev[k][li][0].elapsed_time(lev[k][li][1]) for k in range(args.steps)) * 1e3
+        per_layer.append(dict(name=d.layer.name, K=d.layer.cin, M=d.layer.cout, S=d.layer.spatial,
+                              bh=d.layer.block_h, nnz=d.nnz, row_slots=mode_cfg[d.layer.name],
+                              us=us, gflops=d.flops() / us / 1e3, gbs=d.alg_bytes() / us / 1e3,
+                              hbm_frac=d.alg_bytes() / us / 1e3 / hbm_peak,
+                              alg_bytes=d.alg_bytes(), flops=d.flops()))
+    tot_us = sum(p["us"] for p in per_layer)
+    for p in per_layer:
+        p["share"] = p["us"] / tot_us
+    dom = max(per_layer, key=lambda p: p["us"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom["name"])
+        except Exception:
+            traffic = None
+
+    value = flops_step * dist.world / (ms_step * 1e-3) / 1e9  # aggregate GFLOP/s
+    if dist.rank == 0:
+        log(f"{'layer':6s} {'K':>5s} {'M':>5s} {'S':>6s} {'slots':>5s} {'us':>9s} {'GFLOP/s':>9s} "
+            f"{'GB/s':>8s} {'HBM%':>6s} {'share':>6s}")
+        for p in per_layer:
+            log(f"{p['name']:6s} {p['K']:5d} {p['M']:5d} {p['S']:6d} {p['row_slots']:5d} {p['us']:9.1f} "
+                f"{p['gflops']:9.0f} {p['gbs']:8.0f} {100 * p['hbm_frac']:6.1f} {100 * p['share']:6.1f}")
+        log(f"step {ms_step:.3f} ms; layer kernels sum {tot_us / 1e3:.3f} ms; "
+            f"{value:.0f} GFLOP/s aggregate over {dist.world} GPU(s)")
+        if args.layers_json:
+            json.dump(per_layer, open(args.layers_json, "w"), indent=1)
+
+    # ---- end-to-end: the host-buffer C-ABI call (H2D + kernel + D2H per layer)
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for d in data:
+            a = torch.from_numpy(d.act).pin_memory()
+            o = torch.empty((images, d.layer.cout, d.layer.h, d.layer.w)).pin_memory()
+            host.append((a.numpy(), o.numpy()))
+        h2d = sum(d.act.nbytes + d.bias.nbytes for d in data)
+        d2h = sum(o.nbytes for _, o in host)
+
+        def e2e_step():
+            for (dw, _, _, _, fused, cfgk), d, (a, o) in zip(dev_layers, data, host):
+                sp.spmm_host_batched(dw, a, d.bias, fused, o, cfgk)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        dist.barrier(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        dt = dist.max(dt, device=torch.device("cuda", dev))
+        e2e = {"value": round(flops_step * dist.world / (dt / args.steps) / 1e9, 3),
+               "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(dt / args.steps * 1e3, 3),
+               "path": "spcv_cu_spmm_into_host (pinned host buffers, synchronous per layer)"}
+        # e2e outputs must equal the device path's outputs
+        for (_, _, _, o_dev, _, _), (_, o) in zip(dev_layers, host):
+            if not np.array_equal(o_dev.cpu().numpy().view(np.uint32), o.view(np.uint32)):
+                raise SystemExit("e2e output differs from the device-path output")
+
+    # ---- CPU baseline (rank 0, N=1 only), a bounded sample of the same workload
+    cpu = None
+    if dist.world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        n_img = min(args.cpu_images or images, images)
+        sample = data
+        if n_img < images:
+            sample = [make_layer_data(d.layer, n_img, 1000 * (li + 1)) for li, d in enumerate(data)]
+        kind, flops, times = cpu_reference_run(sample, 3, 1, threads)
+        cpu = {"value": round(flops / statistics.median(times) / 1e9, 3), "unit": "GFLOP/s",
+               "cores": threads, "kind": kind,
+               "sample": f"{n_img} image(s) x all {len(layers)} layers of {args.config} "
+                         f"(= {'the full step' if n_img == images else 'a slice of the step'}), "
+                         f"(layer,image) spmm_into units over {threads} threads, median of 3 passes "
+                         f"after 1 warm-up: {statistics.median(times):.3f}s/pass"}
+
+    if dist.rank == 0:
+        roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(dom["gbs"] / hbm_peak, 4), "traffic": traffic,
+                    "kernel": f"spmm_bcsr_kernel [{dom['name']}: {dom['K']}->{dom['M']} @S={dom['S']}]",
+                    "peak_kind": peak_kind,
+                    "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": round(dom["us"], 2),
+                    "share_of_step": round(dom["share"], 3),
+                    "step_hbm_frac": round(bytes_step / (ms_step * 1e-3) / 1e9 / hbm_peak, 4),
+                    "note": "achieved = SURVEY.md §8d algorithmic bytes / CUDA-event launch time; "
+                            "high-AI layers are bound by the shared-memory gather roof, not HBM"}
+        line = {
+            "metric": "SpMM effective GFLOP/s (2*nnz*N)", "value": round(value, 3),
+            "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config shapes)",
+            "config": {"workload": f"{args.config}: {WORKLOAD_DESC[args.config]}",
+                       "images_per_gpu": images, "global_batch": images * dist.world,
+                       "mode": args.mode, "parallelism": f"dp{dist.world} (image shards, no collective)",
+                       "l2": f"inputs larger than L2: {bytes_step / 1e9:.2f} GB touched per step "
+                             f"per GPU vs 126 MB L2, no explicit flush"},
+            "hbm_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+def run_reference(args, layers, images):
+    """--impl reference: the reference's own CPU spmm_into (oracle/_ref) on all
+    host threads; rank 0 only under torchrun, other ranks exit without work."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_img = min(args.cpu_images or images, images)  # default: the full per-GPU workload
+    sample = [make_layer_data(L, n_img, 1000 * (li + 1)) for li, L in enumerate(layers)]
+    kind, flops, times = cpu_reference_run(sample, args.steps, args.warmup, threads)
+    tot = sum(times)
+    value = flops * len(times) / tot / 1e9  # flops = one step's sample
+    line = {
+        "impl": "reference", "metric": "SpMM effective GFLOP/s (2*nnz*N)", "value": round(value, 3),
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot / len(times) * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded, BASELINE config shapes)",
+        "config": {"workload": f"{args.config}: {WORKLOAD_DESC[args.config]}",
+                   "images_per_gpu": images, "global_batch": images * world,
+                   "sample_images_per_step": n_img},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+                         "sample": f"{n_img} image(s) x all {len(layers)} layers per step, "
+                                   f"(layer,image) units over {threads} threads"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,13 @@ class Oracle:
         return rc, keep.reshape(rows, cols).astype(bool)
 
 
+class RefLayer(ctypes.Structure):
+    _fields_ = [("rows", _i), ("cols", _i), ("block_h", _i), ("row_ptr", _p), ("nrp", _z),
+                ("col_idx", _p), ("nblk", _z), ("values", _p), ("nval", _z), ("images", _i),
+                ("H", _i), ("W", _i), ("act", _p), ("bias", _p), ("act_kind", _i), ("lo", _f),
+                ("hi", _f)]
+
+
 class Ref:
     """The unmodified reference (oracle/_ref/libspcv_ref.so via oracle/ref_shim.cpp)."""
 
@@ -128,6 +135,7 @@ class Ref:
         lib.ref_encode_bcsr.argtypes = [_i, _i, _i, _p, _p, _p, _p, ctypes.POINTER(_z)]
         lib.ref_validate_bcsr.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z]
         lib.ref_generate_mask.argtypes = [_i, _i, _d, _i, _i, ctypes.c_uint32, _p]
+        lib.ref_bench_layers.argtypes = [ctypes.POINTER(RefLayer), _i, _i, _i, _i, ctypes.POINTER(_d)]
         lib.ref_bench_spmm.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z, _i, _i, _i, _p, _p, _i,
                                        _f, _f, _p, _i, _i, _i, ctypes.POINTER(_d)]
         self.lib = lib
@@ -201,6 +209,26 @@ class Ref:
                                      ci.size, _ptr(va), va.size, B, H, W, _ptr(act), _ptr(b), k,
                                      lo, hi, None if out is None else _ptr(out), nthreads, warmups,
                                      reps, secs)
+        assert rc == 0, rc
+        return [secs[i] for i in range(reps)]
+
+
+    def bench_layers(self, layers, nthreads, warmups=0, reps=1):
+        """Timed reference spmm_into over several layers' (weights, act [B][K][H][W],
+        bias, fused) tuples; (layer, image) units over nthreads threads.
+        Returns per-rep seconds."""
+        keep, arr = [], (RefLayer * len(layers))()
+        for j, (m, act, bias, fused) in enumerate(layers):
+            act = _f32(act)
+            B, K, H, W = act.shape
+            rp, ci, va = _u32(m.row_ptr), _u32(m.col_idx), _f32(m.values)
+            b = None if bias is None or len(bias) == 0 else _f32(bias)
+            k, lo, hi = _act(fused)
+            keep += [act, rp, ci, va, b]
+            arr[j] = RefLayer(m.rows, m.cols, m.block_h, _ptr(rp), rp.size, _ptr(ci), ci.size,
+                              _ptr(va), va.size, B, H, W, _ptr(act), _ptr(b), k, lo, hi)
+        secs = (_d * reps)()
+        rc = self.lib.ref_bench_layers(arr, len(layers), nthreads, warmups, reps, secs)
         assert rc == 0, rc
         return [secs[i] for i in range(reps)]
 

@@ -10,6 +10,7 @@
 //   LayoutError -> 1, ShapeError -> 2, FormatError -> 3,
 //   other std::invalid_argument -> 4, anything else -> 5.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -208,6 +209,81 @@ int ref_bench_spmm(int rows, int cols, int block_h, const std::uint32_t* row_ptr
         if (out)
             for (int i = 0; i < images; ++i)
                 std::memcpy(out + i * out_sz, outs[i].data.data(), out_sz * sizeof(float));
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// One layer of a multi-layer CPU benchmark (plain data, filled from Python).
+struct RefLayer {
+    int rows, cols, block_h;
+    const std::uint32_t* row_ptr;
+    std::size_t nrp;
+    const std::uint32_t* col_idx;
+    std::size_t nblk;
+    const float* values;
+    std::size_t nval;
+    int images, H, W;
+    const float* act;   // [images][cols][H*W]
+    const float* bias;  // [rows] or null
+    int act_kind;
+    float lo, hi;
+};
+
+// Timed CPU workload: every (layer, image) pair is one spmm_into call (default
+// MicrokernelConfig, n = block_h); `nthreads` std::threads pull units, longest
+// first, from a shared counter. Objects are built once, outside the timing.
+int ref_bench_layers(const RefLayer* L, int nlayers, int nthreads, int warmups, int reps,
+                     double* secs) {
+    try {
+        struct Unit {
+            int layer, image;
+            double cost;
+        };
+        std::vector<spcv::BcsrMatrix> mats;
+        std::vector<spcv::Activation> fns;
+        std::vector<std::vector<spcv::Tensor>> ins(nlayers), outs(nlayers);
+        std::vector<Unit> units;
+        for (int l = 0; l < nlayers; ++l) {
+            const RefLayer& x = L[l];
+            mats.push_back(make_bcsr(x.rows, x.cols, x.block_h, x.row_ptr, x.nrp, x.col_idx, x.nblk,
+                                     x.values, x.nval));
+            fns.push_back(make_act(x.act_kind, x.lo, x.hi));
+            const std::size_t in_sz = static_cast<std::size_t>(x.cols) * x.H * x.W;
+            for (int i = 0; i < x.images; ++i) {
+                ins[l].emplace_back(x.cols, x.H, x.W, spcv::Layout::CHW);
+                std::memcpy(ins[l].back().data.data(), x.act + i * in_sz, in_sz * sizeof(float));
+                outs[l].emplace_back(x.rows, x.H, x.W, spcv::Layout::CHW);
+                units.push_back({l, i, static_cast<double>(x.nval) * x.H * x.W});
+            }
+        }
+        std::stable_sort(units.begin(), units.end(),
+                         [](const Unit& a, const Unit& b) { return a.cost > b.cost; });
+        if (nthreads < 1) nthreads = 1;
+        auto pass = [&] {
+            std::atomic<std::size_t> next{0};
+            std::vector<std::thread> th;
+            for (int t = 0; t < nthreads; ++t)
+                th.emplace_back([&] {
+                    for (std::size_t u; (u = next.fetch_add(1)) < units.size();) {
+                        const Unit& x = units[u];
+                        const RefLayer& ly = L[x.layer];
+                        spcv::MicrokernelConfig cfg;
+                        cfg.n = ly.block_h;
+                        std::span<const float> b(ly.bias, ly.bias ? static_cast<std::size_t>(ly.rows) : 0);
+                        spcv::spmm_into(mats[x.layer], ins[x.layer][x.image], b, fns[x.layer],
+                                        outs[x.layer][x.image], cfg);
+                    }
+                });
+            for (auto& t : th) t.join();
+        };
+        for (int i = 0; i < warmups; ++i) pass();
+        for (int r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            pass();
+            secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
         return 0;
     } catch (...) {
         return code_of(std::current_exception());
