@@ -21,7 +21,6 @@
 
 using spcvk::kBins;
 using spcvk::kMaxSplit;
-using spcvk::kThreads;
 using spcvk::kWarps;
 
 struct spcv_cu_weights {
@@ -63,14 +62,19 @@ int cuda_fail(cudaError_t e, const char* what) {
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr size_t kTwoCtaSmem = 112 * 1024;
 
+// Shared memory of one CTA: [K+1][T] activation tile (row K = zeros for
+// padded steps) + bias[M].
+size_t smem_bytes(int K, int M, int T) {
+    return static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(M) * 4;
+}
+
 // Smallest G (block rows per warp) whose [K][T] tile (+ bias) fits the budget.
 // G=1 -> T=128, G=2 -> T=64, G=4 -> T=32 columns. Prefer two CTAs per SM.
 int choose_groups(int K, int M) {
     for (int G : {1, 2, 4}) {
-        const size_t smem = static_cast<size_t>(K) * (128 / G) * 4 + static_cast<size_t>(M) * 4;
-        if (smem <= kTwoCtaSmem) return G;
+        if (smem_bytes(K, M, 128 / G) <= kTwoCtaSmem) return G;
     }
-    const size_t smem4 = static_cast<size_t>(K) * 32 * 4 + static_cast<size_t>(M) * 4;
+    const size_t smem4 = smem_bytes(K, M, 32);
     return smem4 <= kSmemLimit ? 4 : 0;
 }
 
@@ -225,9 +229,10 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
                 if (k < brows) {
                     const int br = order[k];
                     hdr[s] = make_uint4(static_cast<uint32_t>(br), nnz[br],
-                                        static_cast<uint32_t>(nch), 0u);
+                                        static_cast<uint32_t>(nch), spcvk::kHeader);
                 } else {
-                    hdr[s] = make_uint4(0xFFFFFFFFu, 0u, static_cast<uint32_t>(nch), 0u);
+                    hdr[s] = make_uint4(spcvk::kNoRow, 0u, static_cast<uint32_t>(nch),
+                                        spcvk::kHeader);
                 }
             }
             ++cur;
@@ -235,11 +240,14 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
                 uint4* ch = stream.data() + cur * CH;
                 for (int s = 0; s < G; ++s) {
                     const int k = g * G + s;
-                    if (k >= brows) continue;
-                    const int br = order[k];
-                    uint32_t off[4] = {0, 0, 0, 0};
-                    float vals[16] = {0};
-                    for (int t = 0; t < 4; ++t) {
+                    // Padding steps read the zero row K with weight -0.0f, which
+                    // leaves any accumulator bit-identical (see spmm_kernel.cuh).
+                    const uint32_t zero_row = static_cast<uint32_t>(cols) * pitch;
+                    uint32_t off[4] = {zero_row, zero_row, zero_row, zero_row};
+                    float vals[16];
+                    for (float& v : vals) v = -0.0f;
+                    const int br = k < brows ? order[k] : -1;
+                    for (int t = 0; t < 4 && br >= 0; ++t) {
                         const uint32_t e = static_cast<uint32_t>(4 * c + t);
                         if (e >= nnz[br]) continue;
                         const uint32_t blk = row_ptr[br] + e;
@@ -333,8 +341,18 @@ extern "C" void spcv_cu_free(spcv_cu_weights* w) { free_weights(w); }
 
 namespace {
 
+struct Geometry {
+    long long ntiles;  // column tiles (grid.x)
+    int split;         // CTAs sharing a tile (grid.y)
+    int nwarps;        // warps per CTA
+    size_t smem;       // dynamic shared memory per CTA
+};
+
+template <typename Kern>
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
+
 template <int BH, int G, bool STRICT, bool VEC>
-int launch_one(const spcvk::KernelArgs& a, long long ntiles, int split, size_t smem,
+int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                cudaStream_t st) {
     auto kern = spcvk::spmm_bcsr_kernel<BH, G, STRICT, VEC>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
@@ -347,32 +365,67 @@ int launch_one(const spcvk::KernelArgs& a, long long ntiles, int split, size_t s
                                        static_cast<int>(kSmemLimit)));
         configured.fetch_or(bit);
     }
-    (void)smem;
-    dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(split));
-    kern<<<grid, kThreads, smem, st>>>(a);
+    // Geometry depends only on (kernel, weights, tile count): cache the last one.
+    static thread_local long long key[5] = {-1, -1, -1, -1, -1};
+    static thread_local Geometry g;
+    const long long k[5] = {ntiles, dev, w->cols, w->rows, w->T};
+    if (!std::equal(k, k + 5, key)) {
+        g = geometry(kern, w, ntiles, sms);
+        std::copy(k, k + 5, key);
+    }
+    dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.split));
+    kern<<<grid, g.nwarps * 32, g.smem, st>>>(a);
     SPCV_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }
 
 template <int BH, int G>
-int launch_g(const spcvk::KernelArgs& a, long long ntiles, int split, size_t smem, bool strict,
-             bool vec, cudaStream_t st) {
+int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
+             bool strict, bool vec, cudaStream_t st) {
     if (strict)
-        return vec ? launch_one<BH, G, true, true>(a, ntiles, split, smem, st)
-                   : launch_one<BH, G, true, false>(a, ntiles, split, smem, st);
-    return vec ? launch_one<BH, G, false, true>(a, ntiles, split, smem, st)
-               : launch_one<BH, G, false, false>(a, ntiles, split, smem, st);
+        return vec ? launch_one<BH, G, true, true>(a, w, nt, sms, st)
+                   : launch_one<BH, G, true, false>(a, w, nt, sms, st);
+    return vec ? launch_one<BH, G, false, true>(a, w, nt, sms, st)
+               : launch_one<BH, G, false, false>(a, w, nt, sms, st);
 }
 
 template <int BH>
-int launch_bh(const spcvk::KernelArgs& a, int G, long long ntiles, int split, size_t smem,
+int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
               bool strict, bool vec, cudaStream_t st) {
-    switch (G) {
-        case 1: return launch_g<BH, 1>(a, ntiles, split, smem, strict, vec, st);
-        case 2: return launch_g<BH, 2>(a, ntiles, split, smem, strict, vec, st);
-        default: return launch_g<BH, 4>(a, ntiles, split, smem, strict, vec, st);
+    switch (w->G) {
+        case 1: return launch_g<BH, 1>(a, w, nt, sms, strict, vec, st);
+        case 2: return launch_g<BH, 2>(a, w, nt, sms, strict, vec, st);
+        default: return launch_g<BH, 4>(a, w, nt, sms, strict, vec, st);
     }
+}
+
+// Warps per CTA and CTAs per tile. Among 4/8/16 warps per CTA, take the
+// one with the most resident warps per SM (occupancy API: shared memory and
+// the kernel's real register count), preferring more, smaller CTAs on ties:
+// each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
+// split tiles across CTAs (row split) until the grid covers the GPU.
+template <typename Kern>
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms) {
+    Geometry g;
+    g.ntiles = ntiles;
+    g.smem = smem_bytes(w->cols, w->rows, w->T);
+    int best = 0, per_sm = 1;
+    g.nwarps = 16;
+    for (int nw : {4, 8, 16}) {
+        int ctas = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)
+            ctas = 0;
+        if (ctas * nw > best) {
+            best = ctas * nw;
+            per_sm = ctas;
+            g.nwarps = nw;
+        }
+    }
+    g.split = 1;
+    while (g.nwarps * g.split * 2 <= kBins && ntiles * g.split < static_cast<long long>(sms) * per_sm)
+        g.split *= 2;
+    return g;
 }
 
 // Argument checks in the order of spmm_into (kernels.cpp:306-322).
@@ -433,19 +486,14 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.hi = hi;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
-    const size_t smem = static_cast<size_t>(w->cols) * w->T * 4 + static_cast<size_t>(w->rows) * 4;
-    // Row split: CTAs sharing a tile, so small batches still fill the GPU.
     const int sms = props_for(dev).sms;
-    const int per_sm = (w->block_h == 1 && smem <= kTwoCtaSmem) ? 2 : 1;
-    int split = 1;
-    while (split < kMaxSplit && ntiles * split < static_cast<long long>(sms) * per_sm) split *= 2;
     const bool vec = (S % 4 == 0) && (reinterpret_cast<uintptr_t>(act) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
     switch (w->block_h) {
-        case 1: return launch_bh<1>(a, w->G, ntiles, split, smem, strict, vec, st);
-        case 2: return launch_bh<2>(a, w->G, ntiles, split, smem, strict, vec, st);
-        default: return launch_bh<4>(a, w->G, ntiles, split, smem, strict, vec, st);
+        case 1: return launch_bh<1>(a, w, ntiles, sms, strict, vec, st);
+        case 2: return launch_bh<2>(a, w, ntiles, sms, strict, vec, st);
+        default: return launch_bh<4>(a, w, ntiles, sms, strict, vec, st);
     }
 }
 

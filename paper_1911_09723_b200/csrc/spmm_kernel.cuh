@@ -33,7 +33,6 @@ namespace spcvk {
 
 constexpr int kWarps = 16;              // warps per CTA
 constexpr int kThreads = kWarps * 32;   // 512
-constexpr int kRing = 3;                // chunks of weight stream in flight per warp
 constexpr int kBins = 128;              // schedule bins = kWarps x kMaxSplit
 constexpr int kMaxSplit = kBins / kWarps;  // max CTAs sharing one column tile (8)
 
@@ -84,33 +83,41 @@ __device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi
     return v;
 }
 
+constexpr uint32_t kHeader = 0xFFFFFFFFu;  // ix.w of a group header chunk
+constexpr uint32_t kNoRow = 0xFFFFFFFFu;   // empty row slot
+
 template <int BH>
 struct Chunk {
-    uint4 ix;       // 4 smem byte offsets (data) | {block_row, count, nchunks, 0} (header)
+    uint4 ix;       // 4 smem byte offsets (data) | {block_row, count, nchunks, kHeader} (header)
     uint4 v[BH];    // 4 steps x BH values, step-major
 };
 
 template <int BH, int G, bool STRICT, bool VEC>
-__global__ void __launch_bounds__(kThreads, (BH == 1 ? 2 : 1))
+__global__ void __launch_bounds__(kThreads, 1)
 spmm_bcsr_kernel(const KernelArgs a) {
     constexpr int LPR = 32 / G;       // lanes per block row
     constexpr int T = LPR * 4;        // virtual columns per tile
     constexpr int CH = G * (1 + BH);  // chunk size in 16 B units
+    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
 
     extern __shared__ __align__(16) float smem[];
-    float* s_act = smem;                                // [K][T]
-    float* s_bias = smem + static_cast<size_t>(a.K) * T; // [M]
+    float* s_act = smem;                                        // [K+1][T], row K = zeros
+    float* s_bias = smem + static_cast<size_t>(a.K + 1) * T;   // [M]
 
     const int tid = threadIdx.x;
+    const int nthreads = blockDim.x;
     const long long n0 = static_cast<long long>(blockIdx.x) * T;
     const long long KS = static_cast<long long>(a.K) * a.S;
 
     // ---- stage bias + the [K][T] activation tile (one HBM pass per byte) ----
     if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += kThreads) cp_async4(s_bias + i, a.bias + i);
+        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
+    for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
+        reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
     if constexpr (VEC) {
-        constexpr int Q = T / 4;              // float4 per tile row
-        constexpr int KSTEP = kThreads / Q;
+        constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
+        const int kstep = nthreads / Q;
         const int q = tid % Q;
         const long long n = n0 + 4 * q;
         const bool valid = n < a.N;           // S % 4 == 0: the quad never straddles images
@@ -119,7 +126,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
             const long long b = n / a.S;
             src = b * KS + (n - b * a.S);
         }
-        for (int k = tid / Q; k < a.K; k += KSTEP) {
+        for (int k = tid / Q; k < a.K; k += kstep) {
             float* dst = s_act + static_cast<size_t>(k) * T + 4 * q;
             if (valid)
                 cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
@@ -127,7 +134,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
                 *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     } else {
-        constexpr int KSTEP = kThreads / T;
+        const int kstep = nthreads / T;       // T divides nthreads (T <= 128)
         const int c = tid % T;
         const long long n = n0 + c;
         const bool valid = n < a.N;
@@ -136,7 +143,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
             const long long b = n / a.S;
             src = b * KS + (n - b * a.S);
         }
-        for (int k = tid / T; k < a.K; k += KSTEP) {
+        for (int k = tid / T; k < a.K; k += kstep) {
             float* dst = s_act + static_cast<size_t>(k) * T + c;
             if (valid)
                 cp_async4(dst, a.act + src + static_cast<long long>(k) * a.S);
@@ -175,9 +182,11 @@ spmm_bcsr_kernel(const KernelArgs a) {
     }
 
     // ---- this warp's contiguous slice of the weight stream ----
-    const int split = gridDim.y;            // CTAs sharing this tile (1,2,4,8)
-    const int per = kMaxSplit / split;      // bins per warp
-    const int bin0 = warp * kMaxSplit + blockIdx.y * per;
+    // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
+    // consecutive schedule bins (balanced by the packer's LPT at every split).
+    const int nwarps = nthreads >> 5;
+    const int per = kBins / (nwarps * gridDim.y);
+    const int bin0 = (blockIdx.y * nwarps + warp) * per;
     uint32_t pos = __ldg(a.bin_beg + bin0);
     const uint32_t end = __ldg(a.bin_beg + bin0 + per);
 
@@ -199,85 +208,91 @@ spmm_bcsr_kernel(const KernelArgs a) {
     Chunk<BH> ring[kRing];
 #pragma unroll
     for (int d = 0; d < kRing; ++d) ring[d] = load(pos + d);
-    auto next = [&]() {
-        const Chunk<BH> cur = ring[0];
-#pragma unroll
-        for (int d = 0; d + 1 < kRing; ++d) ring[d] = ring[d + 1];
-        ring[kRing - 1] = load(pos + kRing);
-        ++pos;
-        return cur;
-    };
 
     cp_async_wait_all();
     __syncthreads();
 
-    const char* s_act_lane = reinterpret_cast<const char*>(s_act) + li * 16;
+    const uint32_t lane_off = static_cast<uint32_t>(li) * 16u;
+    const char* s_bytes = reinterpret_cast<const char*>(s_act);
     const bool have_bias = a.bias != nullptr;
 
-    while (pos < end) {
-        // header chunk: {block_row | ~0u, count, nchunks, 0} per slot
-        const Chunk<BH> h = next();
-        const uint32_t brow = h.ix.x;
-        const int cnt = static_cast<int>(h.ix.y);
-        const int nch = static_cast<int>(h.ix.z);
-        const bool live = brow != 0xFFFFFFFFu;
+    float4 acc[BH];
+#pragma unroll
+    for (int i = 0; i < BH; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t brow = kNoRow;
 
-        float4 acc[BH];
+    auto finish = [&]() {
+        if (brow == kNoRow) return;
 #pragma unroll
         for (int i = 0; i < BH; ++i) {
-            const float b = (live && have_bias) ? s_bias[brow * BH + i] : 0.0f;
-            acc[i] = make_float4(b, b, b, b);
-        }
-
-        for (int c = 0; c < nch; ++c) {
-            const Chunk<BH> d = next();
-            const int lim = cnt - 4 * c;
-            const uint32_t off[4] = {d.ix.x, d.ix.y, d.ix.z, d.ix.w};
-            float wv[4 * BH];
+            const long long row = static_cast<long long>(brow) * BH + i;
+            float4 v = acc[i];
+            v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
+            v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
+            v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
+            v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+            if constexpr (VEC) {
+                if (ovalid[0]) __stcs(reinterpret_cast<float4*>(a.out + obase[0] + row * a.S), v);
+            } else {
+                const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int j = 0; j < BH; ++j) {
-                wv[4 * j + 0] = __uint_as_float(d.v[j].x);
-                wv[4 * j + 1] = __uint_as_float(d.v[j].y);
-                wv[4 * j + 2] = __uint_as_float(d.v[j].z);
-                wv[4 * j + 3] = __uint_as_float(d.v[j].w);
-            }
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (t < lim) {
-                    const float4 x = *reinterpret_cast<const float4*>(s_act_lane + off[t]);
-#pragma unroll
-                    for (int i = 0; i < BH; ++i) {
-                        const float w = wv[t * BH + i];
-                        acc[i].x = madd<STRICT>(acc[i].x, w, x.x);
-                        acc[i].y = madd<STRICT>(acc[i].y, w, x.y);
-                        acc[i].z = madd<STRICT>(acc[i].z, w, x.z);
-                        acc[i].w = madd<STRICT>(acc[i].w, w, x.w);
-                    }
-                }
+                for (int j = 0; j < 4; ++j)
+                    if (ovalid[j]) __stcs(a.out + obase[j] + row * a.S, e[j]);
             }
         }
+    };
 
-        if (live) {
+    // One chunk: a group header (ix.w == kHeader) closes the previous group
+    // and opens the next; a data chunk is 4 unconditional steps. Padding steps
+    // point at the zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc
+    // exactly for every acc (including -0.0), so no predication is needed.
+    auto consume = [&](const Chunk<BH>& cur) {
+        if (cur.ix.w == kHeader) {
+            finish();
+            brow = cur.ix.x;
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
-                const long long row = static_cast<long long>(brow) * BH + i;
-                float4 v = acc[i];
-                v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
-                v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
-                v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
-                v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
-                if constexpr (VEC) {
-                    if (ovalid[0])
-                        __stcs(reinterpret_cast<float4*>(a.out + obase[0] + row * a.S), v);
-                } else {
-                    const float e[4] = {v.x, v.y, v.z, v.w};
+                const float b = (brow != kNoRow && have_bias) ? s_bias[brow * BH + i] : 0.0f;
+                acc[i] = make_float4(b, b, b, b);
+            }
+            return;
+        }
+        const uint32_t off[4] = {cur.ix.x, cur.ix.y, cur.ix.z, cur.ix.w};
+        float4 x[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (ovalid[j]) __stcs(a.out + obase[j] + row * a.S, e[j]);
-                }
+        for (int t = 0; t < 4; ++t)
+            x[t] = *reinterpret_cast<const float4*>(s_bytes + (lane_off + off[t]));
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+#pragma unroll
+            for (int i = 0; i < BH; ++i) {
+                const int f = t * BH + i;  // value index within the chunk (step-major)
+                const uint4& vv = cur.v[f >> 2];
+                const uint32_t wb = (f & 3) == 0 ? vv.x : (f & 3) == 1 ? vv.y : (f & 3) == 2 ? vv.z : vv.w;
+                const float w = __uint_as_float(wb);
+                acc[i].x = madd<STRICT>(acc[i].x, w, x[t].x);
+                acc[i].y = madd<STRICT>(acc[i].y, w, x[t].y);
+                acc[i].z = madd<STRICT>(acc[i].z, w, x[t].z);
+                acc[i].w = madd<STRICT>(acc[i].w, w, x[t].w);
             }
         }
+    };
+
+    // Ring rotation by static unrolling: slot d always holds chunk pos+d at
+    // the top of a round, so no register moves are needed.
+    while (pos + kRing <= end) {
+#pragma unroll
+        for (int d = 0; d < kRing; ++d) {
+            const Chunk<BH> cur = ring[d];
+            ring[d] = load(pos + kRing);
+            ++pos;
+            consume(cur);
+        }
     }
+#pragma unroll
+    for (int d = 0; d < kRing; ++d)
+        if (pos + d < end) consume(ring[d]);
+    finish();
 }
 
 // Device decode of the paper-format streams (per-block-row nnz counts,

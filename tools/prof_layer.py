@@ -1,0 +1,60 @@
+#!/usr/bin/env python3
+"""Run one workload layer's SpMM kernel a few times (for ncu / quick timing).
+
+  python tools/prof_layer.py --config c2-b256 --layer pw7 [--reps 5] [--mode fast]
+
+Prints per-launch CUDA-event times; under ncu use -k regex:spmm_bcsr -s <warmups>.
+"""
+import argparse
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1911_09723_b200 as sp  # noqa: E402
+from paper_1911_09723_b200.workloads import CONFIGS, activation_of, make_layer_data  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2-b256")
+    ap.add_argument("--layer", default="pw7")
+    ap.add_argument("--images", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    layers = {L.name: (i, L) for i, L in enumerate(cfg["layers"]())}
+    li, L = layers[args.layer]
+    images = args.images or cfg["images"]
+    d = make_layer_data(L, images, 1000 * (li + 1))
+    dw = sp.DeviceBcsr(d.weights)
+    a = torch.from_numpy(d.act).cuda()
+    b = torch.from_numpy(d.bias).cuda()
+    o = torch.empty(images, L.cout, L.h, L.w, device="cuda")
+    kc = sp.MicrokernelConfig(n=L.block_h, strict=args.mode == "strict")
+    fused = activation_of(L.act)
+    for _ in range(args.warmup):
+        sp.spmm_batched_into(dw, a, b, fused, o, kc)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sp.spmm_batched_into(dw, a, b, fused, o, kc)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    us = statistics.median(ts)
+    print(f"{args.layer} K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
+          f"median {us:.1f} us  {d.flops() / us / 1e3:.0f} GFLOP/s  {d.alg_bytes() / us / 1e3:.0f} GB/s "
+          f"(alg bytes {d.alg_bytes():.0f})")
+
+
+if __name__ == "__main__":
+    main()
