@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -25,8 +26,10 @@ using spcvk::kWarps;
 
 struct spcv_cu_weights {
     int rows = 0, cols = 0, block_h = 1, brows = 0;
-    int G = 1;           // block rows per warp group
-    int T = 128;         // virtual columns per tile
+    int G = 1;           // block rows per warp group (32 / LPR)
+    int LPR = 32;        // lanes per block row
+    int NF = 4;          // float4 column quads per lane
+    int T = 128;         // virtual columns per tile (LPR * NF * 4)
     int device = 0;
     size_t nblocks = 0;
     size_t nchunks = 0;
@@ -63,19 +66,38 @@ constexpr size_t kSmemLimit = 227 * 1024;
 constexpr size_t kTwoCtaSmem = 112 * 1024;
 
 // Shared memory of one CTA: [K+1][T] activation tile (row K = zeros for
-// padded steps) + bias[M].
+// padded steps) + T int64 output column offsets + bias[M].
 size_t smem_bytes(int K, int M, int T) {
-    return static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(M) * 4;
+    return static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(T) * 8 +
+           static_cast<size_t>(M) * 4;
 }
 
-// Smallest G (block rows per warp) whose [K][T] tile (+ bias) fits the budget.
-// G=1 -> T=128, G=2 -> T=64, G=4 -> T=32 columns. Prefer two CTAs per SM.
-int choose_groups(int K, int M) {
-    for (int G : {1, 2, 4}) {
-        if (smem_bytes(K, M, 128 / G) <= kTwoCtaSmem) return G;
+struct Layout {
+    int LPR, NF, T;
+};
+
+// Tile layout for K input channels. Each lane owns NF float4 quads (16
+// columns for block_h 1/2, 8 for block_h 4, bounded by accumulator
+// registers); the widest tile T whose shared-memory footprint leaves room for
+// two CTAs per SM wins, else the widest that fits one CTA.
+// SPCV_TILE_T=32|64|128 overrides (tuning aid).
+Layout choose_layout(int K, int M, int block_h) {
+    const int NF = block_h == 4 ? 2 : 4;
+    const int lprs_bh12[3] = {8, 4, 2};
+    const int lprs_bh4[3] = {16, 8, 4};
+    const int* lprs = block_h == 4 ? lprs_bh4 : lprs_bh12;
+    if (const char* e = std::getenv("SPCV_TILE_T")) {
+        const int want = std::atoi(e);
+        for (int i = 0; i < 3; ++i)
+            if (lprs[i] * NF * 4 == want && smem_bytes(K, M, want) <= kSmemLimit)
+                return {lprs[i], NF, want};
     }
-    const size_t smem4 = smem_bytes(K, M, 32);
-    return smem4 <= kSmemLimit ? 4 : 0;
+    for (size_t budget : {kTwoCtaSmem, kSmemLimit})
+        for (int i = 0; i < 3; ++i) {
+            const int T = lprs[i] * NF * 4;
+            if (smem_bytes(K, M, T) <= budget) return {lprs[i], NF, T};
+        }
+    return {0, NF, 0};
 }
 
 int bitrev3(int i) { return ((i & 1) << 2) | (i & 2) | ((i & 4) >> 2); }
@@ -158,11 +180,12 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
         }
     }
 
-    const int G = choose_groups(cols, rows);
-    if (G == 0)
+    const Layout lay = choose_layout(cols, rows, block_h);
+    if (lay.LPR == 0)
         return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: input channels " + std::to_string(cols) +
                                               " exceed the shared-memory tile limit");
-    const int T = 128 / G;
+    const int G = 32 / lay.LPR;
+    const int T = lay.T;
     const uint32_t pitch = static_cast<uint32_t>(T) * 4;  // smem bytes per activation row
     const int BH = block_h;
 
@@ -275,6 +298,8 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     w->block_h = block_h;
     w->brows = brows;
     w->G = G;
+    w->LPR = lay.LPR;
+    w->NF = lay.NF;
     w->T = T;
     w->nblocks = nblocks;
     w->nchunks = cur;
@@ -351,10 +376,10 @@ struct Geometry {
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
 
-template <int BH, int G, bool STRICT, bool VEC>
+template <int BH, int LPR, int NF, bool STRICT, bool VEC>
 int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, G, STRICT, VEC>;
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STRICT, VEC>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -380,23 +405,31 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
     return SPCV_OK;
 }
 
-template <int BH, int G>
+template <int BH, int LPR, int NF>
 int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
              bool strict, bool vec, cudaStream_t st) {
     if (strict)
-        return vec ? launch_one<BH, G, true, true>(a, w, nt, sms, st)
-                   : launch_one<BH, G, true, false>(a, w, nt, sms, st);
-    return vec ? launch_one<BH, G, false, true>(a, w, nt, sms, st)
-               : launch_one<BH, G, false, false>(a, w, nt, sms, st);
+        return vec ? launch_one<BH, LPR, NF, true, true>(a, w, nt, sms, st)
+                   : launch_one<BH, LPR, NF, true, false>(a, w, nt, sms, st);
+    return vec ? launch_one<BH, LPR, NF, false, true>(a, w, nt, sms, st)
+               : launch_one<BH, LPR, NF, false, false>(a, w, nt, sms, st);
 }
 
 template <int BH>
 int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
               bool strict, bool vec, cudaStream_t st) {
-    switch (w->G) {
-        case 1: return launch_g<BH, 1>(a, w, nt, sms, strict, vec, st);
-        case 2: return launch_g<BH, 2>(a, w, nt, sms, strict, vec, st);
-        default: return launch_g<BH, 4>(a, w, nt, sms, strict, vec, st);
+    if constexpr (BH == 4) {
+        switch (w->LPR) {
+            case 16: return launch_g<BH, 16, 2>(a, w, nt, sms, strict, vec, st);
+            case 8: return launch_g<BH, 8, 2>(a, w, nt, sms, strict, vec, st);
+            default: return launch_g<BH, 4, 2>(a, w, nt, sms, strict, vec, st);
+        }
+    } else {
+        switch (w->LPR) {
+            case 8: return launch_g<BH, 8, 4>(a, w, nt, sms, strict, vec, st);
+            case 4: return launch_g<BH, 4, 4>(a, w, nt, sms, strict, vec, st);
+            default: return launch_g<BH, 2, 4>(a, w, nt, sms, strict, vec, st);
+        }
     }
 }
 

@@ -92,46 +92,64 @@ struct Chunk {
     uint4 v[BH];    // 4 steps x BH values, step-major
 };
 
-template <int BH, int G, bool STRICT, bool VEC>
+// Lane layout: LPR lanes per block row, G = 32/LPR rows per warp; each lane
+// owns NF float4 column quads of its row (C = 4*NF columns), so a tile is
+// T = LPR*C virtual columns. Within a quarter-warp the NF float4 loads of the
+// G rows are swizzled ((j + gi) mod NF) so every 8-lane phase of an LDS.128
+// touches 8 distinct bank quads (conflict-free for LPR >= 2 when NF % 4 == 0,
+// for LPR >= 4 when NF == 2).
+template <int BH, int LPR, int NF, bool STRICT, bool VEC>
 __global__ void __launch_bounds__(kThreads, 1)
 spmm_bcsr_kernel(const KernelArgs a) {
-    constexpr int LPR = 32 / G;       // lanes per block row
-    constexpr int T = LPR * 4;        // virtual columns per tile
+    constexpr int G = 32 / LPR;       // block rows per warp (row slots)
+    constexpr int T = LPR * NF * 4;   // virtual columns per tile
     constexpr int CH = G * (1 + BH);  // chunk size in 16 B units
     constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
 
     extern __shared__ __align__(16) float smem[];
-    float* s_act = smem;                                        // [K+1][T], row K = zeros
-    float* s_bias = smem + static_cast<size_t>(a.K + 1) * T;   // [M]
+    float* s_act = smem;                                            // [K+1][T], row K = zeros
+    long long* s_col = reinterpret_cast<long long*>(s_act + static_cast<size_t>(a.K + 1) * T);  // [T]
+    float* s_bias = reinterpret_cast<float*>(s_col + T);            // [M]
 
     const int tid = threadIdx.x;
     const int nthreads = blockDim.x;
     const long long n0 = static_cast<long long>(blockIdx.x) * T;
     const long long KS = static_cast<long long>(a.K) * a.S;
+    const long long MS = static_cast<long long>(a.M) * a.S;
 
-    // ---- stage bias + the [K][T] activation tile (one HBM pass per byte) ----
+    // ---- stage bias, column bases and the [K][T] activation tile ----
     if (a.bias != nullptr)
         for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
     for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
         reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
             make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = tid; c < T; c += nthreads) {  // output offset of virtual column n0+c (-1: none)
+        const long long n = n0 + c;
+        long long v = -1;
+        if (n < a.N) {
+            const long long b = n / a.S;
+            v = b * MS + (n - b * a.S);
+        }
+        s_col[c] = v;
+    }
     if constexpr (VEC) {
-        constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
-        const int kstep = nthreads / Q;
-        const int q = tid % Q;
-        const long long n = n0 + 4 * q;
-        const bool valid = n < a.N;           // S % 4 == 0: the quad never straddles images
+        constexpr int Q = T / 4;              // float4 per tile row
+        const long long n = n0 + 4 * (tid % Q);
+        const bool valid = n < a.N;           // S % 4 == 0: a quad never straddles images
         long long src = 0;
         if (valid) {
             const long long b = n / a.S;
             src = b * KS + (n - b * a.S);
         }
-        for (int k = tid / Q; k < a.K; k += kstep) {
-            float* dst = s_act + static_cast<size_t>(k) * T + 4 * q;
-            if (valid)
-                cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
-            else
-                *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (Q <= nthreads) {
+            const int kstep = nthreads / Q;
+            for (int k = tid / Q; k < a.K; k += kstep) {
+                float* dst = s_act + static_cast<size_t>(k) * T + 4 * (tid % Q);
+                if (valid)
+                    cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
+                else
+                    *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     } else {
         const int kstep = nthreads / T;       // T divides nthreads (T <= 128)
@@ -156,30 +174,10 @@ spmm_bcsr_kernel(const KernelArgs a) {
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const int gi = lane / LPR;   // row slot within the group
-    const int li = lane % LPR;   // column quad within the tile
-    const long long nq = n0 + 4 * li;
-    const long long MS = static_cast<long long>(a.M) * a.S;
-    long long obase[VEC ? 1 : 4];
-    bool ovalid[VEC ? 1 : 4];
-    if constexpr (VEC) {
-        ovalid[0] = nq < a.N;
-        obase[0] = 0;
-        if (ovalid[0]) {
-            const long long b = nq / a.S;
-            obase[0] = b * MS + (nq - b * a.S);
-        }
-    } else {
+    const int li = lane % LPR;
+    uint32_t lane_off[NF];       // byte offset of this lane's j-th float4 within a tile row
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const long long n = nq + j;
-            ovalid[j] = n < a.N;
-            obase[j] = 0;
-            if (ovalid[j]) {
-                const long long b = n / a.S;
-                obase[j] = b * MS + (n - b * a.S);
-            }
-        }
-    }
+    for (int j = 0; j < NF; ++j) lane_off[j] = 16u * (li + LPR * ((j + gi) % NF));
 
     // ---- this warp's contiguous slice of the weight stream ----
     // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
@@ -212,32 +210,40 @@ spmm_bcsr_kernel(const KernelArgs a) {
     cp_async_wait_all();
     __syncthreads();
 
-    const uint32_t lane_off = static_cast<uint32_t>(li) * 16u;
     const char* s_bytes = reinterpret_cast<const char*>(s_act);
     const bool have_bias = a.bias != nullptr;
 
-    float4 acc[BH];
+    float4 acc[BH][NF];
 #pragma unroll
-    for (int i = 0; i < BH; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < BH; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t brow = kNoRow;
 
     auto finish = [&]() {
         if (brow == kNoRow) return;
 #pragma unroll
-        for (int i = 0; i < BH; ++i) {
-            const long long row = static_cast<long long>(brow) * BH + i;
-            float4 v = acc[i];
-            v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
-            v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
-            v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
-            v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
-            if constexpr (VEC) {
-                if (ovalid[0]) __stcs(reinterpret_cast<float4*>(a.out + obase[0] + row * a.S), v);
-            } else {
-                const float e[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < NF; ++j) {
+            const int col = static_cast<int>(lane_off[j] >> 2);  // first column of the quad
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (ovalid[j]) __stcs(a.out + obase[j] + row * a.S, e[j]);
+            for (int i = 0; i < BH; ++i) {
+                const long long roff = (static_cast<long long>(brow) * BH + i) * a.S;
+                float4 v = acc[i][j];
+                v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
+                v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
+                v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
+                v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+                if constexpr (VEC) {
+                    const long long o = s_col[col];
+                    if (o >= 0) __stcs(reinterpret_cast<float4*>(a.out + o + roff), v);
+                } else {
+                    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const long long o = s_col[col + q];
+                        if (o >= 0) __stcs(a.out + o + roff, e[q]);
+                    }
+                }
             }
         }
     };
@@ -253,27 +259,31 @@ spmm_bcsr_kernel(const KernelArgs a) {
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
                 const float b = (brow != kNoRow && have_bias) ? s_bias[brow * BH + i] : 0.0f;
-                acc[i] = make_float4(b, b, b, b);
+#pragma unroll
+                for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(b, b, b, b);
             }
             return;
         }
         const uint32_t off[4] = {cur.ix.x, cur.ix.y, cur.ix.z, cur.ix.w};
-        float4 x[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            x[t] = *reinterpret_cast<const float4*>(s_bytes + (lane_off + off[t]));
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
+            float4 x[NF];
+#pragma unroll
+            for (int j = 0; j < NF; ++j)
+                x[j] = *reinterpret_cast<const float4*>(s_bytes + (off[t] + lane_off[j]));
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
                 const int f = t * BH + i;  // value index within the chunk (step-major)
                 const uint4& vv = cur.v[f >> 2];
                 const uint32_t wb = (f & 3) == 0 ? vv.x : (f & 3) == 1 ? vv.y : (f & 3) == 2 ? vv.z : vv.w;
                 const float w = __uint_as_float(wb);
-                acc[i].x = madd<STRICT>(acc[i].x, w, x[t].x);
-                acc[i].y = madd<STRICT>(acc[i].y, w, x[t].y);
-                acc[i].z = madd<STRICT>(acc[i].z, w, x[t].z);
-                acc[i].w = madd<STRICT>(acc[i].w, w, x[t].w);
+#pragma unroll
+                for (int j = 0; j < NF; ++j) {
+                    acc[i][j].x = madd<STRICT>(acc[i][j].x, w, x[j].x);
+                    acc[i][j].y = madd<STRICT>(acc[i][j].y, w, x[j].y);
+                    acc[i][j].z = madd<STRICT>(acc[i][j].z, w, x[j].z);
+                    acc[i][j].w = madd<STRICT>(acc[i][j].w, w, x[j].w);
+                }
             }
         }
     };
