@@ -10,7 +10,7 @@ import ctypes
 import os
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libspcv_cu.so")
+LIB_PATH = os.environ.get("SPCV_CU_LIB") or os.path.join(LIB_DIR, "libspcv_cu.so")
 
 # spcv_status (include/spcv_cu.h)
 OK, ERR_LAYOUT, ERR_SHAPE, ERR_FORMAT, ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = range(7)

@@ -10,18 +10,24 @@
 //
 // B200 mapping:
 //  * The column dimension N = images x H*W ("virtual columns") is cut into
-//    tiles of T = 4*32/G columns; one CTA owns one tile and stages the whole
-//    [K][T] activation block into shared memory once (cp.async, 16 B vectors
-//    when H*W % 4 == 0). Every output row of the tile is then produced from
-//    shared memory, so each activation byte crosses HBM exactly once.
+//    tiles of T columns; a CTA stages the whole [K][T] activation block of a
+//    tile into shared memory once, so each activation byte crosses HBM once,
+//    and every output row of the tile is produced from shared memory.
 //  * A warp works on G block rows at a time (a "row group"); each block row
-//    owns 32/G lanes, each lane owns 4 consecutive virtual columns (float4).
-//    One activation LDS.128 per stored block feeds 4*block_h products.
+//    owns LPR = 32/G lanes and each lane owns NF float4 column quads. One
+//    LDS.128 per stored block per quad feeds 4*block_h products.
 //  * Weights arrive as a per-warp contiguous chunk stream built by the host
 //    packer (row bucketing + LPT, see spcv_cu.cu). Every chunk is 4 steps of
-//    (smem byte offset, block values) for each of the G rows, interleaved so a
-//    warp-wide 16 B load is a single L1 wavefront; a register ring keeps
-//    kRing chunks in flight to cover L2 latency.
+//    (smem byte offset, block values) for each of the G rows; a register ring
+//    keeps chunks in flight to cover L2 latency.
+//  * Two kernels share the row-group executor (struct Exec):
+//      spmm_bcsr_kernel     — one tile per CTA, all warps stage with cp.async
+//                             (any H*W, any alignment);
+//      spmm_bcsr_pipelined  — persistent CTA per SM, one producer warp feeding
+//                             an NS-stage shared-memory ring with bulk async
+//                             copies (cp.async.bulk + mbarrier complete_tx)
+//                             while the consumer warps compute the previous
+//                             tiles (H*W % 4 == 0, 16 B-aligned tensors).
 //  * STRICT uses separately rounded multiply and add (__fmul_rn/__fadd_rn),
 //    reproducing the reference bit-for-bit; !STRICT uses FFMA.
 #pragma once
@@ -31,8 +37,15 @@
 
 namespace spcvk {
 
-constexpr int kWarps = 16;              // warps per CTA
-constexpr int kThreads = kWarps * 32;   // 512
+#ifndef SPCV_MAX_THREADS
+#define SPCV_MAX_THREADS 512
+#endif
+#ifndef SPCV_MIN_BLOCKS
+#define SPCV_MIN_BLOCKS 1
+#endif
+constexpr int kWarps = 16;                  // schedule granularity: warps of the widest CTA
+constexpr int kThreads = SPCV_MAX_THREADS;  // launch bound (CTA sizes 128..kThreads)
+constexpr int kMinBlocks = SPCV_MIN_BLOCKS;
 constexpr int kBins = 128;              // schedule bins = kWarps x kMaxSplit
 constexpr int kMaxSplit = kBins / kWarps;  // max CTAs sharing one column tile (8)
 
@@ -46,6 +59,11 @@ struct KernelArgs {
     int K, M, S;
     int act_kind;            // 0 none, 1 clamp
     float lo, hi;
+    // Tail splitting (kernel 1): CTAs blockIdx.x >= tail_start share their
+    // tile with tail_split - 1 neighbours (each takes a slice of the rows), so
+    // the last, partial wave of tiles still covers every SM.
+    long long tail_start;
+    int tail_split;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -98,129 +116,37 @@ struct Chunk {
 // G rows are swizzled ((j + gi) mod NF) so every 8-lane phase of an LDS.128
 // touches 8 distinct bank quads (conflict-free for LPR >= 2 when NF % 4 == 0,
 // for LPR >= 4 when NF == 2).
+#ifndef SPCV_HOIST
+#define SPCV_HOIST 2
+#endif
+constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of their FMAs
+
 template <int BH, int LPR, int NF, bool STRICT, bool VEC>
-__global__ void __launch_bounds__(kThreads, 1)
-spmm_bcsr_kernel(const KernelArgs a) {
-    constexpr int G = 32 / LPR;       // block rows per warp (row slots)
-    constexpr int T = LPR * NF * 4;   // virtual columns per tile
-    constexpr int CH = G * (1 + BH);  // chunk size in 16 B units
-    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
-
-    extern __shared__ __align__(16) float smem[];
-    float* s_act = smem;                                            // [K+1][T], row K = zeros
-    long long* s_col = reinterpret_cast<long long*>(s_act + static_cast<size_t>(a.K + 1) * T);  // [T]
-    float* s_bias = reinterpret_cast<float*>(s_col + T);            // [M]
-
-    const int tid = threadIdx.x;
-    const int nthreads = blockDim.x;
-    const long long n0 = static_cast<long long>(blockIdx.x) * T;
-    const long long KS = static_cast<long long>(a.K) * a.S;
-    const long long MS = static_cast<long long>(a.M) * a.S;
-
-    // ---- stage bias, column bases and the [K][T] activation tile ----
-    if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
-    for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
-        reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
-            make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = tid; c < T; c += nthreads) {  // output offset of virtual column n0+c (-1: none)
-        const long long n = n0 + c;
-        long long v = -1;
-        if (n < a.N) {
-            const long long b = n / a.S;
-            v = b * MS + (n - b * a.S);
-        }
-        s_col[c] = v;
-    }
-    if constexpr (VEC) {
-        constexpr int Q = T / 4;              // float4 per tile row
-        const long long n = n0 + 4 * (tid % Q);
-        const bool valid = n < a.N;           // S % 4 == 0: a quad never straddles images
-        long long src = 0;
-        if (valid) {
-            const long long b = n / a.S;
-            src = b * KS + (n - b * a.S);
-        }
-        if (Q <= nthreads) {
-            const int kstep = nthreads / Q;
-            for (int k = tid / Q; k < a.K; k += kstep) {
-                float* dst = s_act + static_cast<size_t>(k) * T + 4 * (tid % Q);
-                if (valid)
-                    cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
-                else
-                    *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-    } else {
-        const int kstep = nthreads / T;       // T divides nthreads (T <= 128)
-        const int c = tid % T;
-        const long long n = n0 + c;
-        const bool valid = n < a.N;
-        long long src = 0;
-        if (valid) {
-            const long long b = n / a.S;
-            src = b * KS + (n - b * a.S);
-        }
-        for (int k = tid / T; k < a.K; k += kstep) {
-            float* dst = s_act + static_cast<size_t>(k) * T + c;
-            if (valid)
-                cp_async4(dst, a.act + src + static_cast<long long>(k) * a.S);
-            else
-                *dst = 0.f;
-        }
-    }
-
-    // ---- per-lane geometry ----
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int gi = lane / LPR;   // row slot within the group
-    const int li = lane % LPR;
-    uint32_t lane_off[NF];       // byte offset of this lane's j-th float4 within a tile row
-#pragma unroll
-    for (int j = 0; j < NF; ++j) lane_off[j] = 16u * (li + LPR * ((j + gi) % NF));
-
-    // ---- this warp's contiguous slice of the weight stream ----
-    // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
-    // consecutive schedule bins (balanced by the packer's LPT at every split).
-    const int nwarps = nthreads >> 5;
-    const int per = kBins / (nwarps * gridDim.y);
-    const int bin0 = (blockIdx.y * nwarps + warp) * per;
-    uint32_t pos = __ldg(a.bin_beg + bin0);
-    const uint32_t end = __ldg(a.bin_beg + bin0 + per);
-
-    const uint4* stream = a.stream;
-    auto load = [&](uint32_t c) {
-        Chunk<BH> ch;
-        if (c < end) {
-            const uint4* p = stream + static_cast<size_t>(c) * CH;
-            ch.ix = ldg_stream(p + gi);
-#pragma unroll
-            for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G + j * G + gi);
-        } else {
-            ch.ix = make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
-        }
-        return ch;
-    };
-    Chunk<BH> ring[kRing];
-#pragma unroll
-    for (int d = 0; d < kRing; ++d) ring[d] = load(pos + d);
-
-    cp_async_wait_all();
-    __syncthreads();
-
-    const char* s_bytes = reinterpret_cast<const char*>(s_act);
-    const bool have_bias = a.bias != nullptr;
+struct Exec {
+    static constexpr int G = 32 / LPR;
+    static constexpr int T = LPR * NF * 4;
 
     float4 acc[BH][NF];
-#pragma unroll
-    for (int i = 0; i < BH; ++i)
-#pragma unroll
-        for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t brow = kNoRow;
+    uint32_t lane_off[NF];  // byte offset of this lane's j-th quad within a tile row
+    uint32_t brow;
+    const char* s_bytes;    // current activation tile [K+1][T]
+    const long long* s_col; // its output column offsets [T] (-1: past the end)
+    const float* s_bias;
+    bool have_bias;
 
-    auto finish = [&]() {
+    __device__ __forceinline__ void init(int gi, int li, const float* bias_smem, bool hb) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) lane_off[j] = 16u * (li + LPR * ((j + gi) % NF));
+        brow = kNoRow;
+        s_bias = bias_smem;
+        have_bias = hb;
+#pragma unroll
+        for (int i = 0; i < BH; ++i)
+#pragma unroll
+            for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    __device__ __forceinline__ void finish(const KernelArgs& a) {
         if (brow == kNoRow) return;
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
@@ -246,15 +172,16 @@ spmm_bcsr_kernel(const KernelArgs a) {
                 }
             }
         }
-    };
+        brow = kNoRow;
+    }
 
     // One chunk: a group header (ix.w == kHeader) closes the previous group
     // and opens the next; a data chunk is 4 unconditional steps. Padding steps
     // point at the zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc
     // exactly for every acc (including -0.0), so no predication is needed.
-    auto consume = [&](const Chunk<BH>& cur) {
+    __device__ __forceinline__ void consume(const Chunk<BH>& cur, const KernelArgs& a) {
         if (cur.ix.w == kHeader) {
-            finish();
+            finish(a);
             brow = cur.ix.x;
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
@@ -267,6 +194,9 @@ spmm_bcsr_kernel(const KernelArgs a) {
         const uint32_t off[4] = {cur.ix.x, cur.ix.y, cur.ix.z, cur.ix.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
+            // Keep at most kHoist steps of activation loads in flight per warp
+            // (registers: 4*NF per step); TLP across warps covers the rest.
+            if (t % kHoist == 0 && t > 0) asm volatile("" ::: "memory");
             float4 x[NF];
 #pragma unroll
             for (int j = 0; j < NF; ++j)
@@ -286,7 +216,131 @@ spmm_bcsr_kernel(const KernelArgs a) {
                 }
             }
         }
-    };
+    }
+};
+
+template <int BH, int G>
+__device__ __forceinline__ Chunk<BH> load_chunk(const uint4* stream, uint32_t c, int gi) {
+    constexpr int CH = G * (1 + BH);
+    Chunk<BH> ch;
+    const uint4* p = stream + static_cast<size_t>(c) * CH;
+    ch.ix = ldg_stream(p + gi);
+#pragma unroll
+    for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G + j * G + gi);
+    return ch;
+}
+
+template <int BH>
+__device__ __forceinline__ Chunk<BH> zero_chunk() {
+    Chunk<BH> ch;
+    ch.ix = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
+    return ch;
+}
+
+// Output offset of virtual column n (-1 when n >= N): image b, pixel s ->
+// b*M*S + s; row r adds r*S.
+__device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a) {
+    if (n >= a.N) return -1;
+    const long long b = n / a.S;
+    return b * static_cast<long long>(a.M) * a.S + (n - b * a.S);
+}
+
+// ---------------------------------------------------------------- kernel 1
+// One tile per CTA; all threads stage it with cp.async (16 B when VEC).
+template <int BH, int LPR, int NF, bool STRICT, bool VEC>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+spmm_bcsr_kernel(const KernelArgs a) {
+    using E = Exec<BH, LPR, NF, STRICT, VEC>;
+    constexpr int G = E::G;
+    constexpr int T = E::T;
+    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
+
+    extern __shared__ __align__(16) float smem[];
+    float* s_act = smem;                                            // [K+1][T], row K = zeros
+    long long* s_col = reinterpret_cast<long long*>(s_act + static_cast<size_t>(a.K + 1) * T);  // [T]
+    float* s_bias = reinterpret_cast<float*>(s_col + T);            // [M]
+
+    const int tid = threadIdx.x;
+    const int nthreads = blockDim.x;
+    // (tile, row part): full tiles first, then the tail tiles split tail_split ways
+    long long tile = blockIdx.x;
+    int part = blockIdx.y, nparts = gridDim.y;
+    if (tile >= a.tail_start) {
+        const long long k = tile - a.tail_start;
+        tile = a.tail_start + k / a.tail_split;
+        part = static_cast<int>(k % a.tail_split) * gridDim.y + blockIdx.y;
+        nparts = a.tail_split * gridDim.y;
+    }
+    const long long n0 = tile * T;
+    const long long KS = static_cast<long long>(a.K) * a.S;
+
+    // ---- stage bias, column offsets and the [K][T] activation tile ----
+    if (a.bias != nullptr)
+        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
+    for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
+        reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = tid; c < T; c += nthreads) s_col[c] = col_offset(n0 + c, a);
+    if constexpr (VEC) {
+        constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
+        const long long n = n0 + 4 * (tid % Q);
+        const bool valid = n < a.N;           // S % 4 == 0: a quad never straddles images
+        long long src = 0;
+        if (valid) {
+            const long long b = n / a.S;
+            src = b * KS + (n - b * a.S);
+        }
+        for (int k = tid / Q; k < a.K; k += nthreads / Q) {
+            float* dst = s_act + static_cast<size_t>(k) * T + 4 * (tid % Q);
+            if (valid)
+                cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
+            else
+                *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    } else {
+        const int c = tid % T;                // T divides nthreads (T <= 128)
+        const long long n = n0 + c;
+        const bool valid = n < a.N;
+        long long src = 0;
+        if (valid) {
+            const long long b = n / a.S;
+            src = b * KS + (n - b * a.S);
+        }
+        for (int k = tid / T; k < a.K; k += nthreads / T) {
+            float* dst = s_act + static_cast<size_t>(k) * T + c;
+            if (valid)
+                cp_async4(dst, a.act + src + static_cast<long long>(k) * a.S);
+            else
+                *dst = 0.f;
+        }
+    }
+
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int gi = lane / LPR;
+
+    // ---- this warp's contiguous slice of the weight stream ----
+    // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
+    // consecutive schedule bins (balanced by the packer's LPT at every split).
+    const int per = kBins / ((nthreads >> 5) * nparts);
+    const int bin0 = (part * (nthreads >> 5) + warp) * per;
+    uint32_t pos = __ldg(a.bin_beg + bin0);
+    const uint32_t end = __ldg(a.bin_beg + bin0 + per);
+
+    Chunk<BH> ring[kRing];
+#pragma unroll
+    for (int d = 0; d < kRing; ++d)
+        ring[d] = pos + d < end ? load_chunk<BH, G>(a.stream, pos + d, gi) : zero_chunk<BH>();
+
+    cp_async_wait_all();
+    __syncthreads();
+
+    E ex;
+    ex.init(gi, lane % LPR, s_bias, a.bias != nullptr);
+    ex.s_bytes = reinterpret_cast<const char*>(s_act);
+    ex.s_col = s_col;
 
     // Ring rotation by static unrolling: slot d always holds chunk pos+d at
     // the top of a round, so no register moves are needed.
@@ -294,15 +348,210 @@ spmm_bcsr_kernel(const KernelArgs a) {
 #pragma unroll
         for (int d = 0; d < kRing; ++d) {
             const Chunk<BH> cur = ring[d];
-            ring[d] = load(pos + kRing);
+            ring[d] = pos + kRing < end ? load_chunk<BH, G>(a.stream, pos + kRing, gi) : zero_chunk<BH>();
             ++pos;
-            consume(cur);
+            ex.consume(cur, a);
         }
     }
 #pragma unroll
     for (int d = 0; d < kRing; ++d)
-        if (pos + d < end) consume(ring[d]);
-    finish();
+        if (pos + d < end) ex.consume(ring[d], a);
+    ex.finish(a);
+}
+
+// ---------------------------------------------------------------- kernel 2
+// Persistent, warp-specialised pipeline (H*W % 4 == 0, 16 B-aligned tensors):
+// warps 0..W-1 consume tiles, warp W produces them. The producer fills an
+// NS-stage ring of [K+1][T] tiles with cp.async.bulk row segments completing
+// on the stage's "full" mbarrier (expect_tx = the stage's bytes); consumers
+// wait on "full", compute, and arrive on the stage's "empty" mbarrier. The
+// weight stream is read as one continuous ring across tiles (the same chunk
+// sequence repeats per tile), so L2 latency stays hidden at tile boundaries.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+#ifndef SPCV_PIPE_CONSUMERS
+#define SPCV_PIPE_CONSUMERS 16
+#endif
+constexpr int kPipeConsumers = SPCV_PIPE_CONSUMERS;  // consumer warps per CTA
+constexpr int kPipeThreads = (kPipeConsumers + 1) * 32;
+constexpr int kPipeMaxStages = 4;
+
+template <int BH, int LPR, int NF, bool STRICT>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
+    using E = Exec<BH, LPR, NF, STRICT, true>;
+    constexpr int G = E::G;
+    constexpr int T = E::T;
+    constexpr int kRing = BH == 1 ? 3 : 2;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const size_t act_bytes = static_cast<size_t>(a.K + 1) * T * 4;
+    const size_t stage_bytes = act_bytes + static_cast<size_t>(T) * 8;   // tile + column offsets
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);              // full[NS], empty[NS]
+    float* s_bias = reinterpret_cast<float*>(smem_raw + 2 * kPipeMaxStages * 8);
+    unsigned char* stages = smem_raw + 2 * kPipeMaxStages * 8 +
+                            ((static_cast<size_t>(a.M) * 4 + 127) & ~static_cast<size_t>(127));
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < nstages; ++s) {
+            mbar_init(&bars[s], 1);                       // full: producer's arrive + tx bytes
+            mbar_init(&bars[kPipeMaxStages + s], kPipeConsumers);  // empty: one per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (a.bias != nullptr)
+        for (int i = tid; i < a.M; i += blockDim.x) s_bias[i] = __ldg(a.bias + i);
+    for (int s = 0; s < nstages; ++s) {  // zero rows (never overwritten by copies)
+        float* zr = reinterpret_cast<float*>(stages + s * stage_bytes) + static_cast<size_t>(a.K) * T;
+        for (int i = tid; i < T; i += blockDim.x) zr[i] = 0.f;
+    }
+    __syncthreads();
+
+    const long long KS = static_cast<long long>(a.K) * a.S;
+
+    if (warp == kPipeConsumers) {
+        // ------------------------------------------------------ producer
+        long long i = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int st = static_cast<int>(i % nstages);
+            if (i >= nstages) mbar_wait(&bars[kPipeMaxStages + st], static_cast<uint32_t>((i / nstages - 1) & 1));
+            unsigned char* sb = stages + st * stage_bytes;
+            float* s_act = reinterpret_cast<float*>(sb);
+            long long* s_col = reinterpret_cast<long long*>(sb + act_bytes);
+            const long long n0 = tile * T;
+            const int vc = static_cast<int>(min(static_cast<long long>(T), a.N - n0));  // valid columns
+            if (lane == 0) mbar_expect_tx(&bars[st], static_cast<uint32_t>(a.K) * vc * 4u);
+            __syncwarp();
+            // row segments: columns [c0, c0+len) of one image are contiguous per row k
+            for (int c0 = 0; c0 < vc;) {
+                const long long n = n0 + c0;
+                const long long b = n / a.S;
+                const int s0 = static_cast<int>(n - b * a.S);
+                const int len = min(vc - c0, a.S - s0);
+                const float* src = a.act + b * KS + s0;
+                for (int k = lane; k < a.K; k += 32)
+                    bulk_g2s(s_act + static_cast<size_t>(k) * T + c0, src + static_cast<long long>(k) * a.S,
+                             static_cast<uint32_t>(len) * 4u, &bars[st]);
+                c0 += len;
+            }
+            if (vc < T)  // past the last column: zeros (generic-proxy stores)
+                for (int e = lane; e < a.K * (T - vc); e += 32)
+                    s_act[static_cast<size_t>(e / (T - vc)) * T + vc + e % (T - vc)] = 0.f;
+            for (int c = lane; c < T; c += 32) s_col[c] = col_offset(n0 + c, a);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[st]);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- consumers
+    const int gi = lane / LPR;
+    const int per = kBins / (kPipeConsumers * gridDim.y);
+    const int bin0 = (blockIdx.y * kPipeConsumers + warp) * per;
+    const uint32_t beg = __ldg(a.bin_beg + bin0);
+    const uint32_t end = __ldg(a.bin_beg + bin0 + per);
+    const uint32_t L = end - beg;  // chunks per tile for this warp
+    const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    E ex;
+    ex.init(gi, lane % LPR, s_bias, a.bias != nullptr);
+
+    if (L == 0) {  // no rows for this warp: keep the stage handshake going
+        for (long long i = 0; i < my_tiles; ++i) {
+            const int st = static_cast<int>(i % nstages);
+            mbar_wait(&bars[st], static_cast<uint32_t>((i / nstages) & 1));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[kPipeMaxStages + st]);
+        }
+        return;
+    }
+
+    // continuous chunk sequence: tile after tile, the same L chunks each time
+    const long long total = static_cast<long long>(L) * my_tiles;
+    uint32_t lpos = beg;      // next chunk to load (wraps at end)
+    long long loaded = 0;
+    auto next_load = [&]() {
+        if (loaded >= total) return zero_chunk<BH>();
+        const Chunk<BH> ch = load_chunk<BH, G>(a.stream, lpos, gi);
+        lpos = lpos + 1 == end ? beg : lpos + 1;
+        ++loaded;
+        return ch;
+    };
+    Chunk<BH> ring[kRing];
+#pragma unroll
+    for (int d = 0; d < kRing; ++d) ring[d] = next_load();
+
+    long long tile_i = -1;    // index of the tile being consumed
+    uint32_t cpos = 0;        // position within the tile's L chunks
+    auto step = [&](const Chunk<BH>& cur) {
+        if (cpos == 0) {      // tile boundary: release the old stage, acquire the next
+            if (tile_i >= 0) {
+                ex.finish(a);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars[kPipeMaxStages + static_cast<int>(tile_i % nstages)]);
+            }
+            ++tile_i;
+            const int st = static_cast<int>(tile_i % nstages);
+            mbar_wait(&bars[st], static_cast<uint32_t>((tile_i / nstages) & 1));
+            ex.s_bytes = reinterpret_cast<const char*>(stages + st * stage_bytes);
+            ex.s_col = reinterpret_cast<const long long*>(stages + st * stage_bytes + act_bytes);
+        }
+        ex.consume(cur, a);
+        cpos = cpos + 1 == L ? 0 : cpos + 1;
+    };
+    long long done = 0;
+    while (done + kRing <= total) {
+#pragma unroll
+        for (int d = 0; d < kRing; ++d) {
+            const Chunk<BH> cur = ring[d];
+            ring[d] = next_load();
+            ++done;
+            step(cur);
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < kRing; ++d)
+        if (done + d < total) step(ring[d]);
+    ex.finish(a);
+    __syncwarp();
+    if (lane == 0 && tile_i >= 0) mbar_arrive(&bars[kPipeMaxStages + static_cast<int>(tile_i % nstages)]);
 }
 
 // Device decode of the paper-format streams (per-block-row nnz counts,

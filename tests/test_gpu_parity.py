@@ -465,3 +465,25 @@ def test_kernel_launches_are_counted():
     run_device(sp.encode_bcsr(np.eye(4, dtype=np.float32), 1), np.ones((1, 4, 2, 2), np.float32),
                None, NONE)
     assert sp.launch_count() == n0 + 1
+
+
+# ------------------------------------------- both kernels on the same inputs
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+@pytest.mark.parametrize("case", [
+    ("pw3_b8", Layer("pw3", 128, 128, 56, 56, sparsity=0.9), 8),
+    ("c3_bh4", Layer("c3", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.8, 4), 12),
+    ("c3_bh2", Layer("c3", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.9, 2), 12),
+    ("tail", Layer("tail", 64, 96, 6, 10, sparsity=0.7), 37),       # N % T != 0
+    ("k1024", Layer("k", 1024, 256, 4, 4, sparsity=0.95), 300),     # 1-stage tile -> fallback
+], ids=lambda c: c[0] if isinstance(c, tuple) else c)
+def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, case):
+    """SPCV_PIPELINE forces the persistent bulk-copy pipeline (1) or the
+    one-tile-per-CTA kernel (0); both must equal the oracle bit-for-bit."""
+    monkeypatch.setenv("SPCV_PIPELINE", pipeline)
+    _, layer, images = case
+    d = make_layer_data(layer, images, 4242)
+    got = run_device(d.weights, d.act, d.bias, layer.act)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
+    fast = run_device(d.weights, d.act, d.bias, layer.act, strict=False)
+    check_tolerance(d, fast, want)
