@@ -116,6 +116,14 @@ struct Chunk {
 // G rows are swizzled ((j + gi) mod NF) so every 8-lane phase of an LDS.128
 // touches 8 distinct bank quads (conflict-free for LPR >= 2 when NF % 4 == 0,
 // for LPR >= 4 when NF == 2).
+// Output offset of virtual column n (-1 when n >= N): image b, pixel s ->
+// b*M*S + s; row r adds r*S.
+__device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a) {
+    if (n >= a.N) return -1;
+    const long long b = n / a.S;
+    return b * static_cast<long long>(a.M) * a.S + (n - b * a.S);
+}
+
 #ifndef SPCV_HOIST
 #define SPCV_HOIST 2
 #endif
@@ -128,6 +136,7 @@ struct Exec {
 
     float4 acc[BH][NF];
     uint32_t lane_off[NF];  // byte offset of this lane's j-th quad within a tile row
+    long long ocol[VEC ? NF : 1];  // VEC: output offset of each quad's first column
     uint32_t brow;
     const char* s_bytes;    // current activation tile [K+1][T]
     const long long* s_col; // its output column offsets [T] (-1: past the end)
@@ -146,6 +155,15 @@ struct Exec {
             for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
+    // VEC: per-lane output offsets of the tile starting at virtual column n0
+    // (registers instead of s_col: avoids bank-conflicted 8 B shared loads).
+    __device__ __forceinline__ void set_tile(long long n0, const KernelArgs& a) {
+        if constexpr (VEC) {
+#pragma unroll
+            for (int j = 0; j < NF; ++j) ocol[j] = col_offset(n0 + (lane_off[j] >> 2), a);
+        }
+    }
+
     __device__ __forceinline__ void finish(const KernelArgs& a) {
         if (brow == kNoRow) return;
 #pragma unroll
@@ -160,7 +178,7 @@ struct Exec {
                 v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
                 v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
                 if constexpr (VEC) {
-                    const long long o = s_col[col];
+                    const long long o = ocol[j];
                     if (o >= 0) __stcs(reinterpret_cast<float4*>(a.out + o + roff), v);
                 } else {
                     const float e[4] = {v.x, v.y, v.z, v.w};
@@ -237,14 +255,6 @@ __device__ __forceinline__ Chunk<BH> zero_chunk() {
 #pragma unroll
     for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
     return ch;
-}
-
-// Output offset of virtual column n (-1 when n >= N): image b, pixel s ->
-// b*M*S + s; row r adds r*S.
-__device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a) {
-    if (n >= a.N) return -1;
-    const long long b = n / a.S;
-    return b * static_cast<long long>(a.M) * a.S + (n - b * a.S);
 }
 
 // ---------------------------------------------------------------- kernel 1
@@ -341,6 +351,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
     ex.init(gi, lane % LPR, s_bias, a.bias != nullptr);
     ex.s_bytes = reinterpret_cast<const char*>(s_act);
     ex.s_col = s_col;
+    ex.set_tile(n0, a);
 
     // Ring rotation by static unrolling: slot d always holds chunk pos+d at
     // the top of a round, so no register moves are needed.
@@ -403,7 +414,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 #ifndef SPCV_PIPE_CONSUMERS
-#define SPCV_PIPE_CONSUMERS 16
+#define SPCV_PIPE_CONSUMERS 8
 #endif
 constexpr int kPipeConsumers = SPCV_PIPE_CONSUMERS;  // consumer warps per CTA
 constexpr int kPipeThreads = (kPipeConsumers + 1) * 32;
@@ -532,6 +543,7 @@ spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
             mbar_wait(&bars[st], static_cast<uint32_t>((tile_i / nstages) & 1));
             ex.s_bytes = reinterpret_cast<const char*>(stages + st * stage_bytes);
             ex.s_col = reinterpret_cast<const long long*>(stages + st * stage_bytes + act_bytes);
+            ex.set_tile((blockIdx.x + tile_i * static_cast<long long>(gridDim.x)) * T, a);
         }
         ex.consume(cur, a);
         cpos = cpos + 1 == L ? 0 : cpos + 1;
