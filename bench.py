@@ -30,6 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1911_09723_b200.dist import Dist, shard  # noqa: E402
 from paper_1911_09723_b200.workloads import CONFIGS, activation_of, make_layer_data  # noqa: E402
 
 WORKLOAD_DESC = {
@@ -52,41 +53,6 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
-
-
-# --------------------------------------------------------------- dist glue
-class Dist:
-    def __init__(self, backend):
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-        if self.world > 1:
-            import torch.distributed as dist
-
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend=backend)
-            self.pg = dist
-
-    def barrier(self, device=None):
-        if self.pg:
-            if device is not None:
-                self.pg.barrier(device_ids=[device])
-            else:
-                self.pg.barrier()
-
-    def max(self, x: float, device=None) -> float:
-        if not self.pg:
-            return x
-        import torch
-
-        t = torch.tensor([x], dtype=torch.float64, device=device or "cpu")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
-        return float(t.item())
-
-    def close(self):
-        if self.pg:
-            self.pg.destroy_process_group()
 
 
 # ------------------------------------------------------------- clock probe
@@ -177,6 +143,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="c2-b256", choices=sorted(CONFIGS))
     ap.add_argument("--images", type=int, default=None, help="images per GPU (default: config's)")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling: shard this many images over the ranks instead")
     ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -201,6 +169,11 @@ def main():
     dev = dist.local
     torch.cuda.set_device(dev)
     import paper_1911_09723_b200 as sp
+
+    scaling = "weak"
+    if args.global_batch:  # strong scaling: contiguous image shard per rank
+        b0, b1 = shard(args.global_batch, dist.world, dist.rank)
+        images, scaling = b1 - b0, "strong"
 
     # ---- data: weights identical on every rank, activations per-rank shard
     t0 = time.time()
@@ -280,7 +253,9 @@ def main():
         except Exception:
             traffic = None
 
-    value = flops_step * dist.world / (ms_step * 1e-3) / 1e9  # aggregate GFLOP/s
+    # aggregate GFLOP/s: every rank's FLOPs over the max-over-ranks time
+    flops_all = dist.sum(flops_step, device=torch.device("cuda", dev))
+    value = flops_all / (ms_step * 1e-3) / 1e9
     if dist.rank == 0:
         log(f"{'layer':6s} {'K':>5s} {'M':>5s} {'S':>6s} {'slots':>5s} {'us':>9s} {'GFLOP/s':>9s} "
             f"{'GB/s':>8s} {'HBM%':>6s} {'share':>6s}")
@@ -315,7 +290,7 @@ def main():
             e2e_step()
         dt = time.perf_counter() - t0
         dt = dist.max(dt, device=torch.device("cuda", dev))
-        e2e = {"value": round(flops_step * dist.world / (dt / args.steps) / 1e9, 3),
+        e2e = {"value": round(flops_all / (dt / args.steps) / 1e9, 3),
                "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt / args.steps * 1e3, 3),
                "path": "spcv_cu_spmm_into_host (pinned host buffers, synchronous per layer)"}
@@ -353,10 +328,11 @@ def main():
         line = {
             "metric": "SpMM effective GFLOP/s (2*nnz*N)", "value": round(value, 3),
             "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config shapes)",
             "config": {"workload": f"{args.config}: {WORKLOAD_DESC[args.config]}",
-                       "images_per_gpu": images, "global_batch": images * dist.world,
+                       "images_per_gpu": images,
+                       "global_batch": args.global_batch or images * dist.world,
                        "mode": args.mode, "parallelism": f"dp{dist.world} (image shards, no collective)",
                        "l2": f"inputs larger than L2: {bytes_step / 1e9:.2f} GB touched per step "
                              f"per GPU vs 126 MB L2, no explicit flush"},
