@@ -608,17 +608,31 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     }
 }
 
+// Per-thread device scratch and streams of the host-tensor entry point:
+// copies in (h2d), kernels (k) and copies out (d2h) run on three streams so
+// that chunk c+1 uploads while chunk c computes and chunk c-1 downloads.
 struct HostScratch {
     int device = -1;
-    cudaStream_t stream = nullptr;
+    cudaStream_t h2d = nullptr, k = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_done;
     float* buf = nullptr;
     size_t cap = 0;  // floats
-    ~HostScratch() {
+    void release() {
         if (buf) cudaFree(buf);
-        if (stream) cudaStreamDestroy(stream);
+        for (cudaStream_t* s : {&h2d, &k, &d2h})
+            if (*s) cudaStreamDestroy(*s), *s = nullptr;
+        for (auto& e : ev_in) cudaEventDestroy(e);
+        for (auto& e : ev_done) cudaEventDestroy(e);
+        ev_in.clear();
+        ev_done.clear();
+        buf = nullptr;
+        cap = 0;
     }
+    ~HostScratch() { release(); }
 };
 thread_local HostScratch g_scratch;
+
+constexpr size_t kHostChunkBytes = 48u << 20;  // activations + outputs per pipelined chunk
 
 }  // namespace
 
@@ -653,13 +667,10 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
     SPCV_CUDA(cudaSetDevice(w->device));
     HostScratch& hs = g_scratch;
     if (hs.device != w->device) {
-        if (hs.buf) cudaFree(hs.buf);
-        if (hs.stream) cudaStreamDestroy(hs.stream);
-        hs.buf = nullptr;
-        hs.cap = 0;
-        hs.stream = nullptr;
+        hs.release();
         hs.device = w->device;
-        SPCV_CUDA(cudaStreamCreateWithFlags(&hs.stream, cudaStreamNonBlocking));
+        for (cudaStream_t* st : {&hs.h2d, &hs.k, &hs.d2h})
+            SPCV_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
     }
     // 16 B-aligned sub-buffers: act | out | bias
     auto up4 = [](size_t n) { return (n + 3) & ~static_cast<size_t>(3); };
@@ -674,17 +685,42 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
     float* d_act = hs.buf;
     float* d_out = d_act + up4(n_in);
     float* d_bias = n_bias ? d_out + up4(n_out) : nullptr;
-    SPCV_CUDA(cudaMemcpyAsync(d_act, act, n_in * sizeof(float), cudaMemcpyHostToDevice, hs.stream));
-    if (n_bias)
-        SPCV_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice,
-                                  hs.stream));
-    rc = launch(w, d_act, images, act_h, act_w, d_bias, act_kind, lo, hi, d_out, mode, hs.stream);
-    if (rc) {
-        cudaSetDevice(prev);
-        return rc;
+
+    // Image chunks of ~kHostChunkBytes; each chunk: H2D -> kernel -> D2H.
+    const size_t per_image = S * (static_cast<size_t>(act_c) + out_c) * sizeof(float);
+    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(images, kHostChunkBytes / std::max<size_t>(per_image, 1))));
+    const int nchunks = images > 0 ? (images + chunk - 1) / chunk : 0;
+    while (static_cast<int>(hs.ev_in.size()) < nchunks) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        SPCV_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        SPCV_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        hs.ev_in.push_back(a);
+        hs.ev_done.push_back(b);
     }
-    SPCV_CUDA(cudaMemcpyAsync(out, d_out, n_out * sizeof(float), cudaMemcpyDeviceToHost, hs.stream));
-    SPCV_CUDA(cudaStreamSynchronize(hs.stream));
+    const size_t in_img = S * act_c, out_img = S * out_c;
+    if (n_bias)
+        SPCV_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice, hs.h2d));
+    for (int c = 0; c < nchunks; ++c) {
+        const int i0 = c * chunk, ni = std::min(chunk, images - i0);
+        SPCV_CUDA(cudaMemcpyAsync(d_act + i0 * in_img, act + i0 * in_img, ni * in_img * sizeof(float),
+                                  cudaMemcpyHostToDevice, hs.h2d));
+        SPCV_CUDA(cudaEventRecord(hs.ev_in[c], hs.h2d));
+        SPCV_CUDA(cudaStreamWaitEvent(hs.k, hs.ev_in[c], 0));
+        rc = launch(w, d_act + i0 * in_img, ni, act_h, act_w, d_bias, act_kind, lo, hi,
+                    d_out + i0 * out_img, mode, hs.k);
+        if (rc) {
+            cudaStreamSynchronize(hs.h2d);
+            cudaStreamSynchronize(hs.k);
+            cudaSetDevice(prev);
+            return rc;
+        }
+        SPCV_CUDA(cudaEventRecord(hs.ev_done[c], hs.k));
+        SPCV_CUDA(cudaStreamWaitEvent(hs.d2h, hs.ev_done[c], 0));
+        SPCV_CUDA(cudaMemcpyAsync(out + i0 * out_img, d_out + i0 * out_img, ni * out_img * sizeof(float),
+                                  cudaMemcpyDeviceToHost, hs.d2h));
+    }
+    SPCV_CUDA(cudaStreamSynchronize(hs.d2h));
+    SPCV_CUDA(cudaStreamSynchronize(hs.k));
     cudaSetDevice(prev);
     return SPCV_OK;
 }
