@@ -293,7 +293,7 @@ def main():
         e2e = {"value": round(flops_all / (dt / args.steps) / 1e9, 3),
                "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt / args.steps * 1e3, 3),
-               "path": "spcv_cu_spmm_into_host (pinned host buffers, synchronous per layer)"}
+               "path": "spcv_cu_spmm_into_host per layer (pinned host buffers; image chunks pipelined H2D|kernel|D2H on 3 streams)"}
         # e2e outputs must equal the device path's outputs
         for (_, _, _, o_dev, _, _), (_, o) in zip(dev_layers, host):
             if not np.array_equal(o_dev.cpu().numpy().view(np.uint32), o.view(np.uint32)):
