@@ -181,12 +181,11 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     }
 
     const Layout lay = choose_layout(cols, rows, block_h);
-    if (lay.LPR == 0)
+    if (lay.LPR == 0 || cols >= 0xFFFF)
         return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: input channels " + std::to_string(cols) +
                                               " exceed the shared-memory tile limit");
     const int G = 32 / lay.LPR;
     const int T = lay.T;
-    const uint32_t pitch = static_cast<uint32_t>(T) * 4;  // smem bytes per activation row
     const int BH = block_h;
 
     // paper-format streams
@@ -236,37 +235,36 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
         heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
     }
 
-    const int CH = G * (1 + BH);  // 16 B units per chunk
+    // Chunk = G x 8 B (4 u16 activation-row indices per slot; row `cols` is the
+    // zero row) + BH x G x 16 B values. Headers: {block_row | kNoRow, kHeader}.
+    const size_t CB = static_cast<size_t>(G) * 8 + static_cast<size_t>(BH) * G * 16;
     size_t total = 0;
     for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
-    std::vector<uint4> stream(total * CH, make_uint4(0, 0, 0, 0));
+    std::vector<unsigned char> stream(total * CB + 16, 0);
     std::vector<uint32_t> bin_beg(kBins + 1);
     size_t cur = 0;
+    auto put2 = [&](size_t chunk, int slot, uint32_t a, uint32_t b) {
+        uint32_t* q = reinterpret_cast<uint32_t*>(stream.data() + chunk * CB + slot * 8);
+        q[0] = a;
+        q[1] = b;
+    };
     for (int b = 0; b < kBins; ++b) {
         bin_beg[b] = static_cast<uint32_t>(cur);
         for (int g : bins[b]) {
             const int nch = gchunks[g];
-            uint4* hdr = stream.data() + cur * CH;
             for (int s = 0; s < G; ++s) {
                 const int k = g * G + s;
-                if (k < brows) {
-                    const int br = order[k];
-                    hdr[s] = make_uint4(static_cast<uint32_t>(br), nnz[br],
-                                        static_cast<uint32_t>(nch), spcvk::kHeader);
-                } else {
-                    hdr[s] = make_uint4(spcvk::kNoRow, 0u, static_cast<uint32_t>(nch),
-                                        spcvk::kHeader);
-                }
+                put2(cur, s, k < brows ? static_cast<uint32_t>(order[k]) : spcvk::kNoRow,
+                     spcvk::kHeader);
             }
             ++cur;
             for (int c = 0; c < nch; ++c, ++cur) {
-                uint4* ch = stream.data() + cur * CH;
                 for (int s = 0; s < G; ++s) {
                     const int k = g * G + s;
                     // Padding steps read the zero row K with weight -0.0f, which
                     // leaves any accumulator bit-identical (see spmm_kernel.cuh).
-                    const uint32_t zero_row = static_cast<uint32_t>(cols) * pitch;
-                    uint32_t off[4] = {zero_row, zero_row, zero_row, zero_row};
+                    uint32_t idx[4] = {static_cast<uint32_t>(cols), static_cast<uint32_t>(cols),
+                                       static_cast<uint32_t>(cols), static_cast<uint32_t>(cols)};
                     float vals[16];
                     for (float& v : vals) v = -0.0f;
                     const int br = k < brows ? order[k] : -1;
@@ -274,16 +272,13 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
                         const uint32_t e = static_cast<uint32_t>(4 * c + t);
                         if (e >= nnz[br]) continue;
                         const uint32_t blk = row_ptr[br] + e;
-                        off[t] = col_idx[blk] * pitch;
+                        idx[t] = col_idx[blk];
                         for (int i = 0; i < BH; ++i)
                             vals[t * BH + i] = values[static_cast<size_t>(blk) * BH + i];
                     }
-                    ch[s] = make_uint4(off[0], off[1], off[2], off[3]);
-                    for (int j = 0; j < BH; ++j) {
-                        uint4 u;
-                        std::memcpy(&u, vals + 4 * j, 16);
-                        ch[G + j * G + s] = u;
-                    }
+                    put2(cur, s, idx[0] | (idx[1] << 16), idx[2] | (idx[3] << 16));
+                    for (int j = 0; j < BH; ++j)
+                        std::memcpy(stream.data() + cur * CB + G * 8 + (j * G + s) * 16, vals + 4 * j, 16);
                 }
             }
         }
@@ -308,7 +303,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
         (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
         (rc = upload(&w->d_values, values, nvalues)) ||
-        (rc = upload(&w->d_stream, stream.data(), stream.size())) ||
+        (rc = upload(&w->d_stream, reinterpret_cast<const uint4*>(stream.data()), stream.size() / 16)) ||
         (rc = upload(&w->d_bin_beg, bin_beg.data(), bin_beg.size()))) {
         free_weights(w);
         return rc;

@@ -53,7 +53,7 @@ struct KernelArgs {
     const float* act;        // [images][K][S]
     float* out;              // [images][M][S]
     const float* bias;       // [M] or nullptr
-    const uint4* stream;     // chunk stream, 16 B units
+    const uint4* stream;     // chunk stream (chunk_bytes<BH,G>() per chunk)
     const uint32_t* bin_beg; // kBins + 1 chunk offsets
     long long N;             // images * S
     int K, M, S;
@@ -78,7 +78,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+__device__ __forceinline__ uint2 ldg_stream2(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
     uint4 v;
     asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -101,14 +107,21 @@ __device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi
     return v;
 }
 
-constexpr uint32_t kHeader = 0xFFFFFFFFu;  // ix.w of a group header chunk
+constexpr uint32_t kHeader = 0xFFFFFFFFu;  // ix.y of a group header chunk (two 0xFFFF indices)
 constexpr uint32_t kNoRow = 0xFFFFFFFFu;   // empty row slot
 
+// A chunk as one lane sees it: its row slot's 4 steps. Data: ix = 4 u16
+// activation-row indices (row K = the zero row); header: ix = {block_row,
+// kHeader}. v = 4 steps x BH values, step-major.
 template <int BH>
 struct Chunk {
-    uint4 ix;       // 4 smem byte offsets (data) | {block_row, count, nchunks, kHeader} (header)
-    uint4 v[BH];    // 4 steps x BH values, step-major
+    uint2 ix;
+    uint4 v[BH];
 };
+
+// Bytes of one chunk for G row slots: G x 8 B indices, then BH x G x 16 B values.
+template <int BH, int G>
+__host__ __device__ constexpr int chunk_bytes() { return G * 8 + BH * G * 16; }
 
 // Lane layout: LPR lanes per block row, G = 32/LPR rows per warp; each lane
 // owns NF float4 column quads of its row (C = 4*NF columns), so a tile is
@@ -198,7 +211,7 @@ struct Exec {
     // point at the zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc
     // exactly for every acc (including -0.0), so no predication is needed.
     __device__ __forceinline__ void consume(const Chunk<BH>& cur, const KernelArgs& a) {
-        if (cur.ix.w == kHeader) {
+        if (cur.ix.y == kHeader) {
             finish(a);
             brow = cur.ix.x;
 #pragma unroll
@@ -209,7 +222,9 @@ struct Exec {
             }
             return;
         }
-        const uint32_t off[4] = {cur.ix.x, cur.ix.y, cur.ix.z, cur.ix.w};
+        constexpr int kShift = T == 32 ? 7 : (T == 64 ? 8 : (T == 128 ? 9 : 10));  // log2(T*4)
+        const uint32_t off[4] = {(cur.ix.x & 0xFFFFu) << kShift, (cur.ix.x >> 16) << kShift,
+                                 (cur.ix.y & 0xFFFFu) << kShift, (cur.ix.y >> 16) << kShift};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             // Keep at most kHoist steps of activation loads in flight per warp
@@ -239,19 +254,19 @@ struct Exec {
 
 template <int BH, int G>
 __device__ __forceinline__ Chunk<BH> load_chunk(const uint4* stream, uint32_t c, int gi) {
-    constexpr int CH = G * (1 + BH);
+    constexpr int CB = chunk_bytes<BH, G>();
     Chunk<BH> ch;
-    const uint4* p = stream + static_cast<size_t>(c) * CH;
-    ch.ix = ldg_stream(p + gi);
+    const char* p = reinterpret_cast<const char*>(stream) + static_cast<size_t>(c) * CB;
+    ch.ix = ldg_stream2(p + gi * 8);
 #pragma unroll
-    for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G + j * G + gi);
+    for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G * 8 + (j * G + gi) * 16);
     return ch;
 }
 
 template <int BH>
 __device__ __forceinline__ Chunk<BH> zero_chunk() {
     Chunk<BH> ch;
-    ch.ix = make_uint4(0, 0, 0, 0);
+    ch.ix = make_uint2(0, 0);
 #pragma unroll
     for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
     return ch;
