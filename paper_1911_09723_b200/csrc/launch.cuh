@@ -1,0 +1,203 @@
+// launch.cuh — kernel selection and launch geometry, instantiated per block
+// height by launch_bh{1,2,4}.cu (parallel compilation).
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <string>
+
+#include "spcv_internal.h"
+
+namespace spcv_detail {
+
+using spcvk::kBins;
+
+struct Geometry {
+    long long ntiles;      // column tiles
+    int split;             // CTAs sharing every tile (grid.y)
+    int nwarps;            // warps per CTA
+    size_t smem;           // dynamic shared memory per CTA
+    long long tail_start;  // first tile of the split tail (== ntiles: none)
+    int tail_split;        // CTAs per tail tile (grid.x counts them)
+    long long grid_x;
+};
+
+template <typename Kern>
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
+
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
+int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
+               cudaStream_t st) {
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC>;
+    // cudaFuncSetAttribute is per device; remember which devices are done.
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSmemLimit)));
+        configured.fetch_or(bit);
+    }
+    // Geometry depends only on (kernel, weights, tile count): cache the last one.
+    static thread_local long long key[5] = {-1, -1, -1, -1, -1};
+    static thread_local Geometry g;
+    const long long k[5] = {ntiles, dev, w->cols, w->rows, w->T};
+    if (!std::equal(k, k + 5, key)) {
+        g = geometry(kern, w, ntiles, sms);
+        std::copy(k, k + 5, key);
+    }
+    dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
+    spcvk::KernelArgs at = a;
+    at.tail_start = g.tail_start;
+    at.tail_split = g.tail_split;
+    kern<<<grid, g.nwarps * 32, g.smem, st>>>(at);
+    SPCV_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SPCV_OK;
+}
+
+// Shared memory of the pipelined kernel with `ns` stages.
+inline size_t pipe_smem_bytes(int K, int M, int T, int ns) {
+    const size_t stage = static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(T) * 8;
+    return 2 * spcvk::kPipeMaxStages * 8 + ((static_cast<size_t>(M) * 4 + 127) & ~size_t{127}) +
+           stage * ns;
+}
+
+// Stages of the pipelined kernel that fit (0 when fewer than two do).
+inline int pipe_stages(const spcv_cu_weights* w) {
+    for (int ns = spcvk::kPipeMaxStages; ns >= 2; --ns)
+        if (pipe_smem_bytes(w->cols, w->rows, w->T, ns) <= kSmemLimit) return ns;
+    return 0;
+}
+
+template <int BH, int LPR, int NF, bool STRICT>
+int launch_pipe(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
+                int ns, cudaStream_t st) {
+    auto kern = spcvk::spmm_bcsr_pipelined<BH, LPR, NF, STRICT>;
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
+        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSmemLimit)));
+        configured.fetch_or(bit);
+    }
+    const size_t smem = pipe_smem_bytes(w->cols, w->rows, w->T, ns);
+    const long long grid_x = std::min<long long>(ntiles, sms);
+    dim3 grid(static_cast<unsigned>(grid_x), 1u);
+    kern<<<grid, spcvk::kPipeThreads, smem, st>>>(a, ns, ntiles);
+    SPCV_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SPCV_OK;
+}
+
+template <int BH, int LPR, int NF, int STEPS>
+int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
+             bool strict, bool vec, cudaStream_t st) {
+    // Kernel choice: the one-tile-per-CTA kernel; SPCV_KERNEL=pipe (or
+    // SPCV_PIPELINE=1) selects the bulk-copy pipeline (4-step chunks only).
+    const char* kenv = std::getenv("SPCV_KERNEL");
+    const std::string kind = kenv ? kenv : "";
+    // Pipelined persistent kernel when the tile ring fits >= 2 stages and there
+    // are enough tiles to keep every SM streaming; else one tile per CTA.
+    const int ns = vec ? pipe_stages(w) : 0;
+    const char* env = std::getenv("SPCV_PIPELINE");
+    // Opt-in for now: with 8 consumer warps it trails the tile kernel (profiles/).
+    const bool pipe = ns >= 2 && ((env && std::atoi(env) != 0) || kind == "pipe");
+    if constexpr (STEPS == 4) {
+        if (pipe)
+            return strict ? launch_pipe<BH, LPR, NF, true>(a, w, nt, sms, ns, st)
+                          : launch_pipe<BH, LPR, NF, false>(a, w, nt, sms, ns, st);
+    }
+    if (strict)
+        return vec ? launch_one<BH, LPR, NF, STEPS, true, true>(a, w, nt, sms, st)
+                   : launch_one<BH, LPR, NF, STEPS, true, false>(a, w, nt, sms, st);
+    return vec ? launch_one<BH, LPR, NF, STEPS, false, true>(a, w, nt, sms, st)
+               : launch_one<BH, LPR, NF, STEPS, false, false>(a, w, nt, sms, st);
+}
+
+template <int BH, int LPR, int NF>
+int launch_s(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
+             bool strict, bool vec, cudaStream_t st) {
+    return w->STEPS == 2 ? launch_g<BH, LPR, NF, 2>(a, w, nt, sms, strict, vec, st)
+                         : launch_g<BH, LPR, NF, 4>(a, w, nt, sms, strict, vec, st);
+}
+
+template <int BH>
+int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
+              bool strict, bool vec, cudaStream_t st) {
+    if (BH == 4 || w->NF == 2) {
+        switch (w->LPR) {
+            case 16: return launch_s<BH, 16, 2>(a, w, nt, sms, strict, vec, st);
+            case 8: return launch_s<BH, 8, 2>(a, w, nt, sms, strict, vec, st);
+            default: return launch_s<BH, 4, 2>(a, w, nt, sms, strict, vec, st);
+        }
+    }
+    if constexpr (BH != 4) {
+        switch (w->LPR) {
+            case 8: return launch_s<BH, 8, 4>(a, w, nt, sms, strict, vec, st);
+            case 4: return launch_s<BH, 4, 4>(a, w, nt, sms, strict, vec, st);
+            default: return launch_s<BH, 2, 4>(a, w, nt, sms, strict, vec, st);
+        }
+    }
+    return fail(SPCV_ERR_UNSUPPORTED, "spmm: no kernel for this layout");
+}
+
+// Warps per CTA and CTAs per tile. Among 4/8/16 warps per CTA, take the
+// one with the most resident warps per SM (occupancy API: shared memory and
+// the kernel's real register count), preferring more, smaller CTAs on ties:
+// each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
+// split tiles across CTAs (row split) until the grid covers the GPU.
+template <typename Kern>
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms) {
+    Geometry g;
+    g.ntiles = ntiles;
+    g.smem = smem_bytes(w->cols, w->rows, w->T);
+    int best = 0, per_sm = 1;
+    g.nwarps = 16;
+    const char* env_nw = std::getenv("SPCV_NWARPS");
+    for (int nw : {4, 8, 16}) {
+        if (nw * 32 > spcvk::kThreads) continue;
+        if (env_nw && std::atoi(env_nw) != nw) continue;
+        int ctas = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)
+            ctas = 0;
+        if (ctas * nw > best) {
+            best = ctas * nw;
+            per_sm = ctas;
+            g.nwarps = nw;
+        }
+    }
+    g.split = 1;
+    while (g.nwarps * g.split * 2 <= kBins && ntiles * g.split < static_cast<long long>(sms) * per_sm)
+        g.split *= 2;
+    if (const char* e = std::getenv("SPCV_SPLIT")) {
+        const int want = std::atoi(e);
+        if (want >= 1 && g.nwarps * want <= kBins && (want & (want - 1)) == 0) g.split = want;
+    }
+    // Tail splitting: if the last wave of CTAs is partial, split its tiles
+    // across more CTAs (row slices) so it covers the SMs.
+    g.tail_start = ntiles;
+    g.tail_split = 1;
+    const long long resident = static_cast<long long>(sms) * per_sm;
+    const long long total = ntiles * g.split;
+    const long long full_rounds = total / resident;
+    const long long left = total - full_rounds * resident;  // CTAs in the partial round
+    const char* env_tail = std::getenv("SPCV_TAIL");
+    if (full_rounds >= 1 && left > 0 && !(env_tail && std::atoi(env_tail) == 0)) {
+        int ts = 1;
+        while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
+        if (ts > 1) {
+            g.tail_split = ts;
+            g.tail_start = ntiles - left / g.split;
+        }
+    }
+    g.grid_x = g.tail_start + (ntiles - g.tail_start) * g.tail_split;
+    return g;
+}
+
+
+}  // namespace spcv_detail

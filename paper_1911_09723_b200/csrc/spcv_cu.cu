@@ -17,32 +17,13 @@
 #include <tuple>
 #include <vector>
 
-#include "../../include/spcv_cu.h"
-#include "spmm_kernel.cuh"
+#include "spcv_internal.h"
 
 using spcvk::kBins;
 using spcvk::kMaxSplit;
 using spcvk::kWarps;
 
-struct spcv_cu_weights {
-    int rows = 0, cols = 0, block_h = 1, brows = 0;
-    int G = 1;           // block rows per warp group (32 / LPR)
-    int LPR = 32;        // lanes per block row
-    int NF = 4;          // float4 column quads per lane
-    int T = 128;         // virtual columns per tile (LPR * NF * 4)
-    int device = 0;
-    size_t nblocks = 0;
-    size_t nchunks = 0;
-    // paper-format streams (north_star): counts, deltas, values
-    uint32_t* d_nnz = nullptr;
-    uint32_t* d_delta = nullptr;
-    float* d_values = nullptr;
-    // execution schedule
-    uint4* d_stream = nullptr;
-    uint32_t* d_bin_beg = nullptr;
-};
-
-namespace {
+namespace spcv_detail {
 
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
@@ -56,36 +37,59 @@ int cuda_fail(cudaError_t e, const char* what) {
     return fail(SPCV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define SPCV_CUDA(call)                                  \
-    do {                                                 \
-        cudaError_t e_ = (call);                         \
-        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-    } while (0)
+}  // namespace spcv_detail
 
-constexpr size_t kSmemLimit = 227 * 1024;
-constexpr size_t kTwoCtaSmem = 112 * 1024;
+using namespace spcv_detail;
 
-// Shared memory of one CTA: [K+1][T] activation tile (row K = zeros for
-// padded steps) + T int64 output column offsets + bias[M].
-size_t smem_bytes(int K, int M, int T) {
-    return static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(T) * 8 +
-           static_cast<size_t>(M) * 4;
+namespace spcvk {
+
+// Device decode of the paper-format streams (per-block-row nnz counts,
+// per-block input-channel deltas, values) back into BCSR, for the bit-exact
+// pack/unpack round trip. One thread per block row after a serial prefix over
+// counts (block rows <= a few thousand).
+__global__ void unpack_rowptr_kernel(const uint32_t* nnz, int brows, uint32_t* row_ptr) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        uint32_t acc = 0;
+        row_ptr[0] = 0;
+        for (int r = 0; r < brows; ++r) {
+            acc += nnz[r];
+            row_ptr[r + 1] = acc;
+        }
+    }
 }
+
+__global__ void unpack_cols_kernel(const uint32_t* row_ptr, const uint32_t* delta, int brows,
+                                   uint32_t* col_idx) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= brows) return;
+    uint32_t col = 0;
+    for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
+        col += delta[b];
+        col_idx[b] = col;
+    }
+}
+
+}  // namespace spcvk
+
+namespace {
 
 struct Layout {
     int LPR, NF, T;
 };
 
-// Tile layout for K input channels. Each lane owns NF float4 quads (16
-// columns for block_h 1/2, 8 for block_h 4, bounded by accumulator
-// registers); the widest tile T whose shared-memory footprint leaves room for
-// two CTAs per SM wins, else the widest that fits one CTA.
-// SPCV_TILE_T=32|64|128 overrides (tuning aid).
+// Tile layout for K input channels. Each lane owns NF float4 quads: 8
+// columns (NF=2) for block_h 4 and for K <= 256 (short rows: more warps
+// resident), 16 columns (NF=4) otherwise (halves the weight-stream share of
+// the shared-memory pipe). The widest tile T whose shared-memory footprint
+// leaves room for two CTAs per SM wins, else the widest that fits one CTA.
+// SPCV_NF=2|4 and SPCV_TILE_T=32|64|128 override (tuning aids).
 Layout choose_layout(int K, int M, int block_h) {
-    const int NF = block_h == 4 ? 2 : 4;
-    const int lprs_bh12[3] = {8, 4, 2};
-    const int lprs_bh4[3] = {16, 8, 4};
-    const int* lprs = block_h == 4 ? lprs_bh4 : lprs_bh12;
+    int NF = (block_h == 4 || (block_h == 1 && K <= 256)) ? 2 : 4;
+    if (const char* e = std::getenv("SPCV_NF"))  // tuning aid: 2 or 4 float4 quads per lane
+        if (block_h != 4 && (std::atoi(e) == 2 || std::atoi(e) == 4)) NF = std::atoi(e);
+    const int lprs_nf4[3] = {8, 4, 2};
+    const int lprs_nf2[3] = {16, 8, 4};
+    const int* lprs = NF == 2 ? lprs_nf2 : lprs_nf4;
     if (const char* e = std::getenv("SPCV_TILE_T")) {
         const int want = std::atoi(e);
         for (int i = 0; i < 3; ++i)
@@ -187,6 +191,14 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     const int G = 32 / lay.LPR;
     const int T = lay.T;
     const int BH = block_h;
+    if (brows >= static_cast<int>(spcvk::kNoRow))
+        return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: too many block rows");
+    // Steps per chunk: rows are padded to a multiple of STEPS (zero row,
+    // weight -0.0f) and the max over a row group, so short rows (mean < 16
+    // blocks) use 2-step chunks. SPCV_STEPS=2|4 overrides.
+    int STEPS = nblocks < static_cast<size_t>(16) * brows ? 2 : 4;
+    if (const char* e = std::getenv("SPCV_STEPS"))
+        if (std::atoi(e) == 2 || std::atoi(e) == 4) STEPS = std::atoi(e);
 
     // paper-format streams
     std::vector<uint32_t> nnz(brows), delta(nblocks);
@@ -215,7 +227,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
             const int k = g * G + s;
             if (k < brows) mx = std::max(mx, nnz[order[k]]);
         }
-        gchunks[g] = static_cast<int>((mx + 3) / 4);
+        gchunks[g] = static_cast<int>((mx + STEPS - 1) / STEPS);
     }
     std::vector<std::vector<int>> bins(kBins);
     using Item = std::tuple<long long, int, int>;  // load, priority, bin
@@ -235,18 +247,24 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
         heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
     }
 
-    // Chunk = G x 8 B (4 u16 activation-row indices per slot; row `cols` is the
-    // zero row) + BH x G x 16 B values. Headers: {block_row | kNoRow, kHeader}.
-    const size_t CB = static_cast<size_t>(G) * 8 + static_cast<size_t>(BH) * G * 16;
+    // Chunk (spmm_kernel.cuh, Fmt): index area G x STEPS u16 (padded to 16 B),
+    // value area G x STEPS*BH f32 in 16 B units [unit][slot] (8 B per slot
+    // when STEPS*BH == 2). Headers: first index word kHeaderHi | block_row.
+    const int NI = STEPS / 2, NV = STEPS * BH;
+    const size_t IB = (static_cast<size_t>(G) * NI * 4 + 15) / 16 * 16;
+    const size_t CB = IB + static_cast<size_t>(G) * NV * 4;
     size_t total = 0;
     for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
     std::vector<unsigned char> stream(total * CB + 16, 0);
     std::vector<uint32_t> bin_beg(kBins + 1);
     size_t cur = 0;
-    auto put2 = [&](size_t chunk, int slot, uint32_t a, uint32_t b) {
-        uint32_t* q = reinterpret_cast<uint32_t*>(stream.data() + chunk * CB + slot * 8);
-        q[0] = a;
-        q[1] = b;
+    auto idx_word = [&](size_t chunk, int slot, int wi) -> uint32_t* {
+        return reinterpret_cast<uint32_t*>(stream.data() + chunk * CB + (slot * NI + wi) * 4);
+    };
+    auto val_word = [&](size_t chunk, int slot, int f) -> float* {
+        unsigned char* base = stream.data() + chunk * CB + IB;
+        if (NV == 2) return reinterpret_cast<float*>(base + slot * 8 + f * 4);
+        return reinterpret_cast<float*>(base + ((f / 4) * G + slot) * 16 + (f % 4) * 4);
     };
     for (int b = 0; b < kBins; ++b) {
         bin_beg[b] = static_cast<uint32_t>(cur);
@@ -254,31 +272,28 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
             const int nch = gchunks[g];
             for (int s = 0; s < G; ++s) {
                 const int k = g * G + s;
-                put2(cur, s, k < brows ? static_cast<uint32_t>(order[k]) : spcvk::kNoRow,
-                     spcvk::kHeader);
+                *idx_word(cur, s, 0) =
+                    spcvk::kHeaderHi | (k < brows ? static_cast<uint32_t>(order[k]) : spcvk::kNoRow);
             }
             ++cur;
             for (int c = 0; c < nch; ++c, ++cur) {
                 for (int s = 0; s < G; ++s) {
                     const int k = g * G + s;
-                    // Padding steps read the zero row K with weight -0.0f, which
-                    // leaves any accumulator bit-identical (see spmm_kernel.cuh).
-                    uint32_t idx[4] = {static_cast<uint32_t>(cols), static_cast<uint32_t>(cols),
-                                       static_cast<uint32_t>(cols), static_cast<uint32_t>(cols)};
-                    float vals[16];
-                    for (float& v : vals) v = -0.0f;
                     const int br = k < brows ? order[k] : -1;
-                    for (int t = 0; t < 4 && br >= 0; ++t) {
-                        const uint32_t e = static_cast<uint32_t>(4 * c + t);
-                        if (e >= nnz[br]) continue;
-                        const uint32_t blk = row_ptr[br] + e;
-                        idx[t] = col_idx[blk];
+                    for (int t = 0; t < STEPS; ++t) {
+                        // Padding steps read the zero row K with weight -0.0f, which
+                        // leaves any accumulator bit-identical (see spmm_kernel.cuh).
+                        uint32_t idx = static_cast<uint32_t>(cols);
+                        const uint32_t e = static_cast<uint32_t>(STEPS * c + t);
+                        const bool real = br >= 0 && e < nnz[br];
+                        const uint32_t blk = real ? row_ptr[br] + e : 0;
+                        if (real) idx = col_idx[blk];
+                        uint32_t* w = idx_word(cur, s, t / 2);
+                        *w |= (t & 1) ? (idx << 16) : idx;
                         for (int i = 0; i < BH; ++i)
-                            vals[t * BH + i] = values[static_cast<size_t>(blk) * BH + i];
+                            *val_word(cur, s, t * BH + i) =
+                                real ? values[static_cast<size_t>(blk) * BH + i] : -0.0f;
                     }
-                    put2(cur, s, idx[0] | (idx[1] << 16), idx[2] | (idx[3] << 16));
-                    for (int j = 0; j < BH; ++j)
-                        std::memcpy(stream.data() + cur * CB + G * 8 + (j * G + s) * 16, vals + 4 * j, 16);
                 }
             }
         }
@@ -293,6 +308,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     w->block_h = block_h;
     w->brows = brows;
     w->G = G;
+    w->STEPS = STEPS;
     w->LPR = lay.LPR;
     w->NF = lay.NF;
     w->T = T;
@@ -361,177 +377,6 @@ extern "C" void spcv_cu_free(spcv_cu_weights* w) { free_weights(w); }
 
 namespace {
 
-struct Geometry {
-    long long ntiles;      // column tiles
-    int split;             // CTAs sharing every tile (grid.y)
-    int nwarps;            // warps per CTA
-    size_t smem;           // dynamic shared memory per CTA
-    long long tail_start;  // first tile of the split tail (== ntiles: none)
-    int tail_split;        // CTAs per tail tile (grid.x counts them)
-    long long grid_x;
-};
-
-template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
-
-template <int BH, int LPR, int NF, bool STRICT, bool VEC>
-int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
-               cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STRICT, VEC>;
-    // cudaFuncSetAttribute is per device; remember which devices are done.
-    static std::atomic<uint64_t> configured{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(configured.load() & bit)) {
-        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kSmemLimit)));
-        configured.fetch_or(bit);
-    }
-    // Geometry depends only on (kernel, weights, tile count): cache the last one.
-    static thread_local long long key[5] = {-1, -1, -1, -1, -1};
-    static thread_local Geometry g;
-    const long long k[5] = {ntiles, dev, w->cols, w->rows, w->T};
-    if (!std::equal(k, k + 5, key)) {
-        g = geometry(kern, w, ntiles, sms);
-        std::copy(k, k + 5, key);
-    }
-    dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
-    spcvk::KernelArgs at = a;
-    at.tail_start = g.tail_start;
-    at.tail_split = g.tail_split;
-    kern<<<grid, g.nwarps * 32, g.smem, st>>>(at);
-    SPCV_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return SPCV_OK;
-}
-
-// Shared memory of the pipelined kernel with `ns` stages.
-size_t pipe_smem_bytes(int K, int M, int T, int ns) {
-    const size_t stage = static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(T) * 8;
-    return 2 * spcvk::kPipeMaxStages * 8 + ((static_cast<size_t>(M) * 4 + 127) & ~size_t{127}) +
-           stage * ns;
-}
-
-// Stages of the pipelined kernel that fit (0 when fewer than two do).
-int pipe_stages(const spcv_cu_weights* w) {
-    for (int ns = spcvk::kPipeMaxStages; ns >= 2; --ns)
-        if (pipe_smem_bytes(w->cols, w->rows, w->T, ns) <= kSmemLimit) return ns;
-    return 0;
-}
-
-template <int BH, int LPR, int NF, bool STRICT>
-int launch_pipe(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
-                int ns, cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_pipelined<BH, LPR, NF, STRICT>;
-    static std::atomic<uint64_t> configured{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(configured.load() & bit)) {
-        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kSmemLimit)));
-        configured.fetch_or(bit);
-    }
-    const size_t smem = pipe_smem_bytes(w->cols, w->rows, w->T, ns);
-    const long long grid_x = std::min<long long>(ntiles, sms);
-    dim3 grid(static_cast<unsigned>(grid_x), 1u);
-    kern<<<grid, spcvk::kPipeThreads, smem, st>>>(a, ns, ntiles);
-    SPCV_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return SPCV_OK;
-}
-
-template <int BH, int LPR, int NF>
-int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
-             bool strict, bool vec, cudaStream_t st) {
-    // Pipelined persistent kernel when the tile ring fits >= 2 stages and there
-    // are enough tiles to keep every SM streaming; else one tile per CTA.
-    const int ns = vec ? pipe_stages(w) : 0;
-    const char* env = std::getenv("SPCV_PIPELINE");
-    // Opt-in for now: with 8 consumer warps it trails the tile kernel (profiles/).
-    const bool pipe = ns >= 2 && env && std::atoi(env) != 0 && nt >= 1;
-    if (pipe)
-        return strict ? launch_pipe<BH, LPR, NF, true>(a, w, nt, sms, ns, st)
-                      : launch_pipe<BH, LPR, NF, false>(a, w, nt, sms, ns, st);
-    if (strict)
-        return vec ? launch_one<BH, LPR, NF, true, true>(a, w, nt, sms, st)
-                   : launch_one<BH, LPR, NF, true, false>(a, w, nt, sms, st);
-    return vec ? launch_one<BH, LPR, NF, false, true>(a, w, nt, sms, st)
-               : launch_one<BH, LPR, NF, false, false>(a, w, nt, sms, st);
-}
-
-template <int BH>
-int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
-              bool strict, bool vec, cudaStream_t st) {
-    if constexpr (BH == 4) {
-        switch (w->LPR) {
-            case 16: return launch_g<BH, 16, 2>(a, w, nt, sms, strict, vec, st);
-            case 8: return launch_g<BH, 8, 2>(a, w, nt, sms, strict, vec, st);
-            default: return launch_g<BH, 4, 2>(a, w, nt, sms, strict, vec, st);
-        }
-    } else {
-        switch (w->LPR) {
-            case 8: return launch_g<BH, 8, 4>(a, w, nt, sms, strict, vec, st);
-            case 4: return launch_g<BH, 4, 4>(a, w, nt, sms, strict, vec, st);
-            default: return launch_g<BH, 2, 4>(a, w, nt, sms, strict, vec, st);
-        }
-    }
-}
-
-// Warps per CTA and CTAs per tile. Among 4/8/16 warps per CTA, take the
-// one with the most resident warps per SM (occupancy API: shared memory and
-// the kernel's real register count), preferring more, smaller CTAs on ties:
-// each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
-// split tiles across CTAs (row split) until the grid covers the GPU.
-template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms) {
-    Geometry g;
-    g.ntiles = ntiles;
-    g.smem = smem_bytes(w->cols, w->rows, w->T);
-    int best = 0, per_sm = 1;
-    g.nwarps = 16;
-    const char* env_nw = std::getenv("SPCV_NWARPS");
-    for (int nw : {4, 8, 16}) {
-        if (nw * 32 > spcvk::kThreads) continue;
-        if (env_nw && std::atoi(env_nw) != nw) continue;
-        int ctas = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)
-            ctas = 0;
-        if (ctas * nw > best) {
-            best = ctas * nw;
-            per_sm = ctas;
-            g.nwarps = nw;
-        }
-    }
-    g.split = 1;
-    while (g.nwarps * g.split * 2 <= kBins && ntiles * g.split < static_cast<long long>(sms) * per_sm)
-        g.split *= 2;
-    if (const char* e = std::getenv("SPCV_SPLIT")) {
-        const int want = std::atoi(e);
-        if (want >= 1 && g.nwarps * want <= kBins && (want & (want - 1)) == 0) g.split = want;
-    }
-    // Tail splitting: if the last wave of CTAs is partial, split its tiles
-    // across more CTAs (row slices) so it covers the SMs.
-    g.tail_start = ntiles;
-    g.tail_split = 1;
-    const long long resident = static_cast<long long>(sms) * per_sm;
-    const long long total = ntiles * g.split;
-    const long long full_rounds = total / resident;
-    const long long left = total - full_rounds * resident;  // CTAs in the partial round
-    const char* env_tail = std::getenv("SPCV_TAIL");
-    if (full_rounds >= 1 && left > 0 && !(env_tail && std::atoi(env_tail) == 0)) {
-        int ts = 1;
-        while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
-        if (ts > 1) {
-            g.tail_split = ts;
-            g.tail_start = ntiles - left / g.split;
-        }
-    }
-    g.grid_x = g.tail_start + (ntiles - g.tail_start) * g.tail_split;
-    return g;
-}
-
 // Argument checks in the order of spmm_into (kernels.cpp:306-322).
 int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, int act_h,
                int act_w, size_t bias_len, int act_kind, float lo, float hi, int out_layout,
@@ -597,9 +442,9 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
     switch (w->block_h) {
-        case 1: return launch_bh<1>(a, w, ntiles, sms, strict, vec, st);
-        case 2: return launch_bh<2>(a, w, ntiles, sms, strict, vec, st);
-        default: return launch_bh<4>(a, w, ntiles, sms, strict, vec, st);
+        case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);
+        case 2: return launch_bh2(a, w, ntiles, sms, strict, vec, st);
+        default: return launch_bh4(a, w, ntiles, sms, strict, vec, st);
     }
 }
 

@@ -53,7 +53,7 @@ struct KernelArgs {
     const float* act;        // [images][K][S]
     float* out;              // [images][M][S]
     const float* bias;       // [M] or nullptr
-    const uint4* stream;     // chunk stream (chunk_bytes<BH,G>() per chunk)
+    const uint4* stream;     // chunk stream (chunk_bytes_g<BH,STEPS>(G) bytes per chunk)
     const uint32_t* bin_beg; // kBins + 1 chunk offsets
     long long N;             // images * S
     int K, M, S;
@@ -73,6 +73,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
@@ -107,21 +110,37 @@ __device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi
     return v;
 }
 
-constexpr uint32_t kHeader = 0xFFFFFFFFu;  // ix.y of a group header chunk (two 0xFFFF indices)
-constexpr uint32_t kNoRow = 0xFFFFFFFFu;   // empty row slot
+constexpr uint32_t kNoRow = 0xFFFFu;       // empty row slot (block rows < 65535)
+constexpr uint32_t kHeaderHi = 0xFFFF0000u; // header word: kHeaderHi | block_row
 
-// A chunk as one lane sees it: its row slot's 4 steps. Data: ix = 4 u16
-// activation-row indices (row K = the zero row); header: ix = {block_row,
-// kHeader}. v = 4 steps x BH values, step-major.
-template <int BH>
-struct Chunk {
-    uint2 ix;
-    uint4 v[BH];
+// Chunk format, STEPS (2 or 4) steps per row slot:
+//   index area: G slots x STEPS u16 activation-row indices (row K = the zero
+//               row), padded to 16 B; a header's first word is
+//               kHeaderHi | block_row (an index word's high half is <= K < 0xFFFF);
+//   value area: G slots x STEPS*BH f32, step-major per slot; stored in 16 B
+//               units [unit][slot] when STEPS*BH >= 4 (each warp-wide load is
+//               contiguous), else 8 B per slot.
+template <int BH, int STEPS>
+struct Fmt {
+    static constexpr int NI = STEPS / 2;      // 32-bit index words per slot
+    static constexpr int NV = STEPS * BH;     // 32-bit value words per slot
+    template <int G>
+    __host__ __device__ static constexpr int idx_bytes() { return (G * NI * 4 + 15) / 16 * 16; }
+    template <int G>
+    __host__ __device__ static constexpr int bytes() { return idx_bytes<G>() + G * NV * 4; }
 };
 
-// Bytes of one chunk for G row slots: G x 8 B indices, then BH x G x 16 B values.
-template <int BH, int G>
-__host__ __device__ constexpr int chunk_bytes() { return G * 8 + BH * G * 16; }
+template <int BH, int STEPS>
+__host__ __device__ constexpr int chunk_bytes_g(int G) {
+    return (G * (STEPS / 2) * 4 + 15) / 16 * 16 + G * STEPS * BH * 4;
+}
+
+// A chunk as one lane sees it (its row slot).
+template <int BH, int STEPS>
+struct Chunk {
+    uint32_t ix[STEPS / 2];
+    uint32_t v[STEPS * BH];
+};
 
 // Lane layout: LPR lanes per block row, G = 32/LPR rows per warp; each lane
 // owns NF float4 column quads of its row (C = 4*NF columns), so a tile is
@@ -138,11 +157,11 @@ __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a
 }
 
 #ifndef SPCV_HOIST
-#define SPCV_HOIST 2
+#define SPCV_HOIST 4
 #endif
 constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of their FMAs
 
-template <int BH, int LPR, int NF, bool STRICT, bool VEC>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
 struct Exec {
     static constexpr int G = 32 / LPR;
     static constexpr int T = LPR * NF * 4;
@@ -162,6 +181,13 @@ struct Exec {
         brow = kNoRow;
         s_bias = bias_smem;
         have_bias = hb;
+#pragma unroll
+        for (int i = 0; i < BH; ++i)
+#pragma unroll
+            for (int j = 0; j < NF; ++j) acc[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    __device__ __forceinline__ void reset() {
 #pragma unroll
         for (int i = 0; i < BH; ++i)
 #pragma unroll
@@ -206,14 +232,14 @@ struct Exec {
         brow = kNoRow;
     }
 
-    // One chunk: a group header (ix.w == kHeader) closes the previous group
-    // and opens the next; a data chunk is 4 unconditional steps. Padding steps
-    // point at the zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc
-    // exactly for every acc (including -0.0), so no predication is needed.
-    __device__ __forceinline__ void consume(const Chunk<BH>& cur, const KernelArgs& a) {
-        if (cur.ix.y == kHeader) {
+    // One chunk: a group header closes the previous group and opens the next;
+    // a data chunk is STEPS unconditional steps. Padding steps point at the
+    // zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc exactly for
+    // every acc (including -0.0), so no predication is needed.
+    __device__ __forceinline__ void consume(const Chunk<BH, STEPS>& cur, const KernelArgs& a) {
+        if ((cur.ix[0] & kHeaderHi) == kHeaderHi) {
             finish(a);
-            brow = cur.ix.x;
+            brow = cur.ix[0] & 0xFFFFu;
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
                 const float b = (brow != kNoRow && have_bias) ? s_bias[brow * BH + i] : 0.0f;
@@ -223,23 +249,18 @@ struct Exec {
             return;
         }
         constexpr int kShift = T == 32 ? 7 : (T == 64 ? 8 : (T == 128 ? 9 : 10));  // log2(T*4)
-        const uint32_t off[4] = {(cur.ix.x & 0xFFFFu) << kShift, (cur.ix.x >> 16) << kShift,
-                                 (cur.ix.y & 0xFFFFu) << kShift, (cur.ix.y >> 16) << kShift};
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            // Keep at most kHoist steps of activation loads in flight per warp
-            // (registers: 4*NF per step); TLP across warps covers the rest.
-            if (t % kHoist == 0 && t > 0) asm volatile("" ::: "memory");
+        for (int t = 0; t < STEPS; ++t) {
+            if (kHoist < STEPS && t % kHoist == 0 && t > 0) __syncwarp();
+            const uint32_t word = cur.ix[t >> 1];
+            const uint32_t off = ((t & 1) ? (word >> 16) : (word & 0xFFFFu)) << kShift;
             float4 x[NF];
 #pragma unroll
             for (int j = 0; j < NF; ++j)
-                x[j] = *reinterpret_cast<const float4*>(s_bytes + (off[t] + lane_off[j]));
+                x[j] = *reinterpret_cast<const float4*>(s_bytes + (off + lane_off[j]));
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
-                const int f = t * BH + i;  // value index within the chunk (step-major)
-                const uint4& vv = cur.v[f >> 2];
-                const uint32_t wb = (f & 3) == 0 ? vv.x : (f & 3) == 1 ? vv.y : (f & 3) == 2 ? vv.z : vv.w;
-                const float w = __uint_as_float(wb);
+                const float w = __uint_as_float(cur.v[t * BH + i]);
 #pragma unroll
                 for (int j = 0; j < NF; ++j) {
                     acc[i][j].x = madd<STRICT>(acc[i][j].x, w, x[j].x);
@@ -252,61 +273,54 @@ struct Exec {
     }
 };
 
-template <int BH, int G>
-__device__ __forceinline__ Chunk<BH> load_chunk(const uint4* stream, uint32_t c, int gi) {
-    constexpr int CB = chunk_bytes<BH, G>();
-    Chunk<BH> ch;
+template <int BH, int G, int STEPS>
+__device__ __forceinline__ Chunk<BH, STEPS> load_chunk(const uint4* stream, uint32_t c, int gi) {
+    using F = Fmt<BH, STEPS>;
+    constexpr int CB = F::template bytes<G>();
+    Chunk<BH, STEPS> ch;
     const char* p = reinterpret_cast<const char*>(stream) + static_cast<size_t>(c) * CB;
-    ch.ix = ldg_stream2(p + gi * 8);
-#pragma unroll
-    for (int j = 0; j < BH; ++j) ch.v[j] = ldg_stream(p + G * 8 + (j * G + gi) * 16);
-    return ch;
-}
-
-template <int BH>
-__device__ __forceinline__ Chunk<BH> zero_chunk() {
-    Chunk<BH> ch;
-    ch.ix = make_uint2(0, 0);
-#pragma unroll
-    for (int j = 0; j < BH; ++j) ch.v[j] = make_uint4(0, 0, 0, 0);
-    return ch;
-}
-
-// ---------------------------------------------------------------- kernel 1
-// One tile per CTA; all threads stage it with cp.async (16 B when VEC).
-template <int BH, int LPR, int NF, bool STRICT, bool VEC>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-spmm_bcsr_kernel(const KernelArgs a) {
-    using E = Exec<BH, LPR, NF, STRICT, VEC>;
-    constexpr int G = E::G;
-    constexpr int T = E::T;
-    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
-
-    extern __shared__ __align__(16) float smem[];
-    float* s_act = smem;                                            // [K+1][T], row K = zeros
-    long long* s_col = reinterpret_cast<long long*>(s_act + static_cast<size_t>(a.K + 1) * T);  // [T]
-    float* s_bias = reinterpret_cast<float*>(s_col + T);            // [M]
-
-    const int tid = threadIdx.x;
-    const int nthreads = blockDim.x;
-    // (tile, row part): full tiles first, then the tail tiles split tail_split ways
-    long long tile = blockIdx.x;
-    int part = blockIdx.y, nparts = gridDim.y;
-    if (tile >= a.tail_start) {
-        const long long k = tile - a.tail_start;
-        tile = a.tail_start + k / a.tail_split;
-        part = static_cast<int>(k % a.tail_split) * gridDim.y + blockIdx.y;
-        nparts = a.tail_split * gridDim.y;
+    if constexpr (F::NI == 1) {
+        asm volatile("ld.global.nc.u32 %0, [%1];\n" : "=r"(ch.ix[0]) : "l"(p + gi * 4));
+    } else {
+        const uint2 v = ldg_stream2(p + gi * 8);
+        ch.ix[0] = v.x;
+        ch.ix[1] = v.y;
     }
-    const long long n0 = tile * T;
-    const long long KS = static_cast<long long>(a.K) * a.S;
+    const char* pv = p + F::template idx_bytes<G>();
+    if constexpr (F::NV == 2) {
+        const uint2 v = ldg_stream2(pv + gi * 8);
+        ch.v[0] = v.x;
+        ch.v[1] = v.y;
+    } else {
+#pragma unroll
+        for (int u = 0; u < F::NV / 4; ++u) {
+            const uint4 v = ldg_stream(pv + (u * G + gi) * 16);
+            ch.v[4 * u + 0] = v.x;
+            ch.v[4 * u + 1] = v.y;
+            ch.v[4 * u + 2] = v.z;
+            ch.v[4 * u + 3] = v.w;
+        }
+    }
+    return ch;
+}
 
-    // ---- stage bias, column offsets and the [K][T] activation tile ----
-    if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
-    for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
-        reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
-            make_float4(0.f, 0.f, 0.f, 0.f);
+template <int BH, int STEPS>
+__device__ __forceinline__ Chunk<BH, STEPS> zero_chunk() {
+    Chunk<BH, STEPS> ch;
+#pragma unroll
+    for (int j = 0; j < STEPS / 2; ++j) ch.ix[j] = 0;
+#pragma unroll
+    for (int j = 0; j < STEPS * BH; ++j) ch.v[j] = 0;
+    return ch;
+}
+
+// Issue the cp.async copies of tile [n0, n0+T) into s_act [K][T] (16 B when
+// VEC, 4 B otherwise; zeros past column N) and write its column offsets.
+// Completion: cp.async.wait_all by the issuing threads, then a CTA barrier.
+template <int T, bool VEC>
+__device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long long n0,
+                                           const KernelArgs& a, int tid, int nthreads) {
+    const long long KS = static_cast<long long>(a.K) * a.S;
     for (int c = tid; c < T; c += nthreads) s_col[c] = col_offset(n0 + c, a);
     if constexpr (VEC) {
         constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
@@ -341,6 +355,43 @@ spmm_bcsr_kernel(const KernelArgs a) {
                 *dst = 0.f;
         }
     }
+}
+
+// ---------------------------------------------------------------- kernel 1
+// One tile per CTA; all threads stage it with cp.async (16 B when VEC).
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+spmm_bcsr_kernel(const KernelArgs a) {
+    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC>;
+    constexpr int G = E::G;
+    constexpr int T = E::T;
+    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
+
+    extern __shared__ __align__(16) float smem[];
+    float* s_act = smem;                                            // [K+1][T], row K = zeros
+    long long* s_col = reinterpret_cast<long long*>(s_act + static_cast<size_t>(a.K + 1) * T);  // [T]
+    float* s_bias = reinterpret_cast<float*>(s_col + T);            // [M]
+
+    const int tid = threadIdx.x;
+    const int nthreads = blockDim.x;
+    // (tile, row part): full tiles first, then the tail tiles split tail_split ways
+    long long tile = blockIdx.x;
+    int part = blockIdx.y, nparts = gridDim.y;
+    if (tile >= a.tail_start) {
+        const long long k = tile - a.tail_start;
+        tile = a.tail_start + k / a.tail_split;
+        part = static_cast<int>(k % a.tail_split) * gridDim.y + blockIdx.y;
+        nparts = a.tail_split * gridDim.y;
+    }
+    const long long n0 = tile * T;
+
+    // ---- stage bias, zero row, column offsets and the [K][T] activation tile ----
+    if (a.bias != nullptr)
+        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
+    for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
+        reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+    stage_tile<T, VEC>(s_act, s_col, n0, a, tid, nthreads);
 
     const int lane = tid & 31;
     const int warp = tid >> 5;
@@ -354,10 +405,10 @@ spmm_bcsr_kernel(const KernelArgs a) {
     uint32_t pos = __ldg(a.bin_beg + bin0);
     const uint32_t end = __ldg(a.bin_beg + bin0 + per);
 
-    Chunk<BH> ring[kRing];
+    Chunk<BH, STEPS> ring[kRing];
 #pragma unroll
     for (int d = 0; d < kRing; ++d)
-        ring[d] = pos + d < end ? load_chunk<BH, G>(a.stream, pos + d, gi) : zero_chunk<BH>();
+        ring[d] = pos + d < end ? load_chunk<BH, G, STEPS>(a.stream, pos + d, gi) : zero_chunk<BH, STEPS>();
 
     cp_async_wait_all();
     __syncthreads();
@@ -373,8 +424,9 @@ spmm_bcsr_kernel(const KernelArgs a) {
     while (pos + kRing <= end) {
 #pragma unroll
         for (int d = 0; d < kRing; ++d) {
-            const Chunk<BH> cur = ring[d];
-            ring[d] = pos + kRing < end ? load_chunk<BH, G>(a.stream, pos + kRing, gi) : zero_chunk<BH>();
+            const Chunk<BH, STEPS> cur = ring[d];
+            ring[d] = pos + kRing < end ? load_chunk<BH, G, STEPS>(a.stream, pos + kRing, gi)
+                                        : zero_chunk<BH, STEPS>();
             ++pos;
             ex.consume(cur, a);
         }
@@ -438,7 +490,8 @@ constexpr int kPipeMaxStages = 4;
 template <int BH, int LPR, int NF, bool STRICT>
 __global__ void __launch_bounds__(kPipeThreads, 1)
 spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
-    using E = Exec<BH, LPR, NF, STRICT, true>;
+    constexpr int STEPS = 4;
+    using E = Exec<BH, LPR, NF, STEPS, STRICT, true>;
     constexpr int G = E::G;
     constexpr int T = E::T;
     constexpr int kRing = BH == 1 ? 3 : 2;
@@ -534,19 +587,19 @@ spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
     uint32_t lpos = beg;      // next chunk to load (wraps at end)
     long long loaded = 0;
     auto next_load = [&]() {
-        if (loaded >= total) return zero_chunk<BH>();
-        const Chunk<BH> ch = load_chunk<BH, G>(a.stream, lpos, gi);
+        if (loaded >= total) return zero_chunk<BH, STEPS>();
+        const Chunk<BH, STEPS> ch = load_chunk<BH, G, STEPS>(a.stream, lpos, gi);
         lpos = lpos + 1 == end ? beg : lpos + 1;
         ++loaded;
         return ch;
     };
-    Chunk<BH> ring[kRing];
+    Chunk<BH, STEPS> ring[kRing];
 #pragma unroll
     for (int d = 0; d < kRing; ++d) ring[d] = next_load();
 
     long long tile_i = -1;    // index of the tile being consumed
     uint32_t cpos = 0;        // position within the tile's L chunks
-    auto step = [&](const Chunk<BH>& cur) {
+    auto step = [&](const Chunk<BH, STEPS>& cur) {
         if (cpos == 0) {      // tile boundary: release the old stage, acquire the next
             if (tile_i >= 0) {
                 ex.finish(a);
@@ -567,7 +620,7 @@ spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
     while (done + kRing <= total) {
 #pragma unroll
         for (int d = 0; d < kRing; ++d) {
-            const Chunk<BH> cur = ring[d];
+            const Chunk<BH, STEPS> cur = ring[d];
             ring[d] = next_load();
             ++done;
             step(cur);
@@ -579,32 +632,6 @@ spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
     ex.finish(a);
     __syncwarp();
     if (lane == 0 && tile_i >= 0) mbar_arrive(&bars[kPipeMaxStages + static_cast<int>(tile_i % nstages)]);
-}
-
-// Device decode of the paper-format streams (per-block-row nnz counts,
-// per-block input-channel deltas, values) back into BCSR, for the bit-exact
-// pack/unpack round trip. One thread per block row after a serial prefix over
-// counts (block rows <= a few thousand).
-__global__ void unpack_rowptr_kernel(const uint32_t* nnz, int brows, uint32_t* row_ptr) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        uint32_t acc = 0;
-        row_ptr[0] = 0;
-        for (int r = 0; r < brows; ++r) {
-            acc += nnz[r];
-            row_ptr[r + 1] = acc;
-        }
-    }
-}
-
-__global__ void unpack_cols_kernel(const uint32_t* row_ptr, const uint32_t* delta, int brows,
-                                   uint32_t* col_idx) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= brows) return;
-    uint32_t col = 0;
-    for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
-        col += delta[b];
-        col_idx[b] = col;
-    }
 }
 
 }  // namespace spcvk

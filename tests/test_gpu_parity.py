@@ -468,6 +468,7 @@ def test_kernel_launches_are_counted():
 
 
 # ------------------------------------------- both kernels on the same inputs
+@pytest.mark.parametrize("layout", ["default", "steps2", "steps4", "nf2", "nf4_steps2"])
 @pytest.mark.parametrize("pipeline", ["0", "1"])
 @pytest.mark.parametrize("case", [
     ("pw3_b8", Layer("pw3", 128, 128, 56, 56, sparsity=0.9), 8),
@@ -476,10 +477,16 @@ def test_kernel_launches_are_counted():
     ("tail", Layer("tail", 64, 96, 6, 10, sparsity=0.7), 37),       # N % T != 0
     ("k1024", Layer("k", 1024, 256, 4, 4, sparsity=0.95), 300),     # 1-stage tile -> fallback
 ], ids=lambda c: c[0] if isinstance(c, tuple) else c)
-def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, case):
+def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, case, layout):
     """SPCV_PIPELINE forces the persistent bulk-copy pipeline (1) or the
-    one-tile-per-CTA kernel (0); both must equal the oracle bit-for-bit."""
+    one-tile-per-CTA kernel (0); SPCV_STEPS / SPCV_NF force the chunk length
+    and lane width the packer would otherwise pick. Every combination must
+    equal the oracle bit-for-bit."""
     monkeypatch.setenv("SPCV_PIPELINE", pipeline)
+    env = {"steps2": {"SPCV_STEPS": "2"}, "steps4": {"SPCV_STEPS": "4"}, "nf2": {"SPCV_NF": "2"},
+           "nf4_steps2": {"SPCV_NF": "4", "SPCV_STEPS": "2"}}.get(layout, {})
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     _, layer, images = case
     d = make_layer_data(layer, images, 4242)
     got = run_device(d.weights, d.act, d.bias, layer.act)
