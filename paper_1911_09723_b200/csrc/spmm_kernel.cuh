@@ -177,7 +177,8 @@ struct Exec {
 
     __device__ __forceinline__ void init(int gi, int li, const float* bias_smem, bool hb) {
 #pragma unroll
-        for (int j = 0; j < NF; ++j) lane_off[j] = 16u * (li + LPR * ((j + gi) % NF));
+        for (int j = 0; j < NF; ++j)  // LPR >= 8: a phase is one row, no swizzle needed
+            lane_off[j] = 16u * (li + LPR * (LPR >= 8 ? j : (j + gi) % NF));
         brow = kNoRow;
         s_bias = bias_smem;
         have_bias = hb;
@@ -255,9 +256,16 @@ struct Exec {
             const uint32_t word = cur.ix[t >> 1];
             const uint32_t off = ((t & 1) ? (word >> 16) : (word & 0xFFFFu)) << kShift;
             float4 x[NF];
+            if constexpr (LPR >= 8) {  // quads at fixed strides: one address, immediate offsets
+                const char* row = s_bytes + (off + lane_off[0]);
 #pragma unroll
-            for (int j = 0; j < NF; ++j)
-                x[j] = *reinterpret_cast<const float4*>(s_bytes + (off + lane_off[j]));
+                for (int j = 0; j < NF; ++j)
+                    x[j] = *reinterpret_cast<const float4*>(row + 16 * LPR * j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < NF; ++j)
+                    x[j] = *reinterpret_cast<const float4*>(s_bytes + (off + lane_off[j]));
+            }
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
                 const float w = __uint_as_float(cur.v[t * BH + i]);
