@@ -78,13 +78,14 @@ struct Layout {
 };
 
 // Tile layout for K input channels. Each lane owns NF float4 quads: 8
-// columns (NF=2) for block_h 4 and for K < 64 (very short rows, HBM-bound:
-// more warps resident), 16 columns (NF=4) otherwise (halves the weight-stream share of
+// columns (NF=2) for block_h 4 and for layers with few output rows (M <= 96:
+// little work per staged tile, so more resident warps/CTAs matter more),
+// 16 columns (NF=4) otherwise (halves the weight-stream share of the pipe) (halves the weight-stream share of
 // the shared-memory pipe). The widest tile T whose shared-memory footprint
 // leaves room for two CTAs per SM wins, else the widest that fits one CTA.
 // SPCV_NF=2|4 and SPCV_TILE_T=32|64|128 override (tuning aids).
 Layout choose_layout(int K, int M, int block_h) {
-    int NF = (block_h == 4 || (block_h == 1 && K < 64)) ? 2 : 4;
+    int NF = (block_h == 4 || M <= 96) ? 2 : 4;
     if (const char* e = std::getenv("SPCV_NF"))  // tuning aid: 2 or 4 float4 quads per lane
         if (block_h != 4 && (std::atoi(e) == 2 || std::atoi(e) == 4)) NF = std::atoi(e);
     const int lprs_nf4[3] = {8, 4, 2};
