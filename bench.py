@@ -232,6 +232,29 @@ def main():
     ms_total = dist.max(ms_local, device=torch.device("cuda", dev))
     ms_step = ms_total / args.steps
 
+    # The other arithmetic mode on the same packed weights (reported beside the
+    # headline, which is the mode selected by --mode): strict = bit-exact,
+    # fast = FFMA within the north_star tolerance.
+    other = "fast" if args.mode == "strict" else "strict"
+    alt_cfgs = [sp.MicrokernelConfig(n=c.n, strict=(other == "strict")) for (_, _, _, _, _, c) in dev_layers]
+
+    def step_alt():
+        for (dw, a, b, o, fused, _), cfgk in zip(dev_layers, alt_cfgs):
+            sp.spmm_batched_into(dw, a, b, fused, o, cfgk, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step_alt()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier(dev)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_alt()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_alt = dist.max(e0.elapsed_time(e1), device=torch.device("cuda", dev)) / args.steps
+
     # per-layer kernel times (events on the launch stream, averaged over steps)
     per_layer = []
     for li, d in enumerate(data):
@@ -315,6 +338,10 @@ def main():
                          f"(layer,image) spmm_into units over {threads} threads, median of 3 passes "
                          f"after 1 warm-up: {statistics.median(times):.3f}s/pass"}
 
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_sum = clk.summary()
+    f_clk = (clk_sum.get("sm_mhz") or clk_sum.get("sm_max_mhz") or 1965.0) * 1e6
+    gather_roof = sms * 64 * f_clk / 1e12  # TFLOP/s
     if dist.rank == 0:
         roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(dom["gbs"] / hbm_peak, 4), "traffic": traffic,
@@ -323,8 +350,14 @@ def main():
                     "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": round(dom["us"], 2),
                     "share_of_step": round(dom["share"], 3),
                     "step_hbm_frac": round(bytes_step / (ms_step * 1e-3) / 1e9 / hbm_peak, 4),
-                    "note": "achieved = SURVEY.md §8d algorithmic bytes / CUDA-event launch time; "
-                            "high-AI layers are bound by the shared-memory gather roof, not HBM"}
+                    "gather_roof_tflops": round(gather_roof, 2),
+                    "gather_frac": round(dom["gflops"] / 1e3 / gather_roof, 4),
+                    "step_gather_frac": round(value / 1e3 / dist.world / gather_roof, 4),
+                    "note": "achieved = SURVEY.md §8d algorithmic bytes / CUDA-event launch time. "
+                            "Layers with AI > ~2.9 FLOP/B are bound by the shared-memory gather roof "
+                            "(one 4 B activation per stored block per column at 128 B/clk/SM: "
+                            "SMs x 64 FLOP/clk x SM clock), not HBM; gather_frac is against that roof "
+                            "at the clock measured during the run"}
         line = {
             "metric": "SpMM effective GFLOP/s (2*nnz*N)", "value": round(value, 3),
             "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -339,6 +372,11 @@ def main():
             "hbm_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
+            "modes": {args.mode: {"value": round(value, 3), "ms_per_step": round(ms_step, 4)},
+                      other: {"value": round(flops_all / (ms_alt * 1e-3) / 1e9, 3),
+                              "ms_per_step": round(ms_alt, 4)},
+                      "note": "strict = bit-exact vs the reference CPU kernel (default); "
+                              "fast = FFMA, within the north_star nnz-scaled 1e-5 tolerance"},
         }
         print(json.dumps(line), flush=True)
     dist.close()
