@@ -317,7 +317,11 @@ def main():
                "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(dt / args.steps * 1e3, 3),
                "path": "spcv_cu_spmm_into_host per layer (pinned host buffers; image chunks pipelined H2D|kernel|D2H on 3 streams)"}
-        # e2e outputs must equal the device path's outputs
+        # e2e outputs must equal the device path's outputs (re-run one step of
+        # the headline mode: the alternate-mode timing overwrote the outputs)
+        with torch.cuda.stream(stream):
+            step()
+        torch.cuda.synchronize()
         for (_, _, _, o_dev, _, _), (_, o) in zip(dev_layers, host):
             if not np.array_equal(o_dev.cpu().numpy().view(np.uint32), o.view(np.uint32)):
                 raise SystemExit("e2e output differs from the device-path output")
