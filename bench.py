@@ -148,6 +148,7 @@ def main():
     ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the cuBLAS dense fp32 baseline")
     ap.add_argument("--cpu-images", type=int, default=None, help="CPU baseline sample, images")
     ap.add_argument("--layers-json", default=None, help="write per-layer results here")
     args = ap.parse_args()
@@ -290,6 +291,54 @@ def main():
         if args.layers_json:
             json.dump(per_layer, open(args.layers_json, "w"), indent=1)
 
+    # ---- dense fp32 baseline (reference dense_gemm_into, bench.cpp:216-227): the
+    # same layers with dense weights through cuBLAS SGEMM (pedantic fp32)
+    dense = None
+    if not args.no_dense:
+        dws = [torch.from_numpy(d.dense).to(dev) for d in data]
+        dcfg = sp.MicrokernelConfig()
+
+        def step_dense(evs=None):
+            for li, ((_, a, b, o, fused, _), w) in enumerate(zip(dev_layers, dws)):
+                if evs is not None:
+                    evs[li][0].record(stream)
+                sp.dense_gemm_batched_into(w, a, b, fused, o, dcfg, stream=stream)
+                if evs is not None:
+                    evs[li][1].record(stream)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                step_dense()
+            dsteps = max(1, min(args.steps, 5))
+            dev_ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in dws]
+                      for _ in range(dsteps)]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier(dev)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for k in range(dsteps):
+                step_dense(dev_ev[k])
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms_dense = dist.max(e0.elapsed_time(e1), device=torch.device("cuda", dev)) / dsteps
+        dense_flops = sum(2.0 * d.layer.cout * d.layer.cin * d.images * d.layer.spatial for d in data)
+        for li, p in enumerate(per_layer):
+            p["dense_us"] = statistics.mean(dev_ev[k][li][0].elapsed_time(dev_ev[k][li][1])
+                                            for k in range(dsteps)) * 1e3
+        dense = {"ms_per_step": round(ms_dense, 4),
+                 "dense_gflops": round(dense_flops * dist.world / (ms_dense * 1e-3) / 1e9, 1),
+                 "sparse_effective_gflops": round(dense_flops * dist.world / (ms_step * 1e-3) / 1e9, 1),
+                 "sparse_speedup_vs_dense": round(ms_dense / ms_step, 3),
+                 "per_layer_speedup": {p["name"]: round(p["dense_us"] / p["us"], 2) for p in per_layer},
+                 "how": "cuBLAS SGEMM strided-batched (CUBLAS_PEDANTIC_MATH) + bias/clamp epilogue, "
+                        f"same inputs, {dsteps} steps"}
+        del dws
+        with torch.cuda.stream(stream):
+            step()  # restore the sparse outputs for the e2e check below
+        torch.cuda.synchronize()
+        if dist.rank == 0:
+            log(f"dense fp32 baseline: {ms_dense:.3f} ms/step; sparse speedup {ms_dense / ms_step:.2f}x")
+
     # ---- end-to-end: the host-buffer C-ABI call (H2D + kernel + D2H per layer)
     e2e = None
     if not args.no_e2e:
@@ -374,7 +423,7 @@ def main():
                        "l2": f"inputs larger than L2: {bytes_step / 1e9:.2f} GB touched per step "
                              f"per GPU vs 126 MB L2, no explicit flush"},
             "hbm_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "dense_baseline": dense,
             "gpu_launches": launches, "clocks": clk.summary(),
             "modes": {args.mode: {"value": round(value, 3), "ms_per_step": round(ms_step, 4)},
                       other: {"value": round(flops_all / (ms_alt * 1e-3) / 1e9, 3),

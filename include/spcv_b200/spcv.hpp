@@ -154,6 +154,13 @@ inline Tensor spconv_1x1(const BcsrMatrix& w, const Tensor& act, std::span<const
     return spmm(w, act, bias, fused, cfg);
 }
 
+/// kernels.hpp:85-90: dense baseline with the same contract (host tensors;
+/// cuBLAS SGEMM in pedantic fp32 + bias/clamp epilogue, not bit-exact).
+void dense_gemm_into(const DenseMatrix& w, const Tensor& act, std::span<const float> bias,
+                     const Activation& fused, Tensor& out, const MicrokernelConfig& cfg = {});
+Tensor dense_gemm_baseline(const DenseMatrix& w, const Tensor& act, std::span<const float> bias,
+                           const Activation& fused = {}, const MicrokernelConfig& cfg = {});
+
 // ------------------------------------------------------- device-resident
 /// Weights packed once onto the current CUDA device (RAII over spcv_cu_weights).
 class DeviceBcsr {

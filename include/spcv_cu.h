@@ -105,6 +105,20 @@ int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_l
                            int out_layout, int out_c, int out_h, int out_w, int cfg_m, int cfg_n,
                            int mode);
 
+/* Dense fp32 baseline with the same contract as the SpMM entry point: the
+ * reference's dense_gemm_into (kernels.hpp:85-90, kernels.cpp:345-373), its
+ * in-repo speed baseline for the sparse kernel (bench.cpp:216-227). `w` is a
+ * DEVICE rows x cols row-major matrix; act/out/bias are device tensors as in
+ * spcv_cu_spmm_into. Computed by cuBLAS SGEMM (pedantic fp32, no TF32) plus a
+ * fused bias+clamp epilogue kernel: not bit-exact (cuBLAS's summation order),
+ * within fp32 rounding of the dense oracle. Checks in the reference order
+ * (kernels.cpp:347-360): layout -> cols -> bias -> out shape -> strip width. */
+int spcv_cu_dense_gemm_into(const float* w, int rows, int cols, const float* act, int act_layout,
+                            int images, int act_c, int act_h, int act_w, const float* bias,
+                            size_t bias_len, int act_kind, float lo, float hi, float* out,
+                            int out_layout, int out_c, int out_h, int out_w, int cfg_m,
+                            void* stream);
+
 /* Number of SpMM kernel launches issued by this library so far (process-wide). */
 uint64_t spcv_cu_launch_count(void);
 

@@ -19,6 +19,7 @@ from .spmm import (
     Tier,
     decode_bcsr,
     default_strip_width,
+    dense_gemm_batched_into,
     encode_bcsr,
     parse_tier,
     parse_variant,
@@ -32,7 +33,7 @@ from .spmm import (
 )
 
 __all__ = [
-    "Activation", "BcsrMatrix", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
+    "Activation", "BcsrMatrix", "dense_gemm_batched_into", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
     "LayoutError", "MicrokernelConfig", "ShapeError", "Tensor", "Tier", "decode_bcsr",
     "default_strip_width", "encode_bcsr", "parse_tier", "parse_variant", "resolve_tier",
     "spconv_1x1", "spmm", "spmm_batched_into", "spmm_host_batched", "spmm_into",

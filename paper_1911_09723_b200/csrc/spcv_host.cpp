@@ -10,6 +10,8 @@
 //   spmm allocating wrapper            src/kernels.cpp:336-341
 #include "spcv_b200/spcv.hpp"
 
+#include <cuda_runtime.h>
+
 #include <cstdlib>
 #include <string_view>
 
@@ -248,6 +250,59 @@ Tensor spmm(const BcsrMatrix& w, const Tensor& act, std::span<const float> bias,
             const Activation& fused, const MicrokernelConfig& cfg) {
     Tensor out(w.rows, act.height, act.width, Layout::CHW);
     spmm_into(w, act, bias, fused, out, cfg);
+    return out;
+}
+
+void dense_gemm_into(const DenseMatrix& w, const Tensor& act, std::span<const float> bias,
+                     const Activation& fused, Tensor& out, const MicrokernelConfig& cfg) {
+    // kernels.cpp:347-360 order, checked here so errors precede any device work
+    if (act.layout != Layout::CHW) throw LayoutError("dense_gemm: activation must be CHW");
+    if (w.cols != act.channels) throw ShapeError("dense_gemm: weight cols != activation channels");
+    if (!bias.empty() && static_cast<int>(bias.size()) != w.rows)
+        throw ShapeError("dense_gemm: bias length != rows");
+    if (out.layout != Layout::CHW || out.channels != w.rows || out.height != act.height ||
+        out.width != act.width)
+        throw ShapeError("dense_gemm: output tensor shape/layout mismatch");
+    const int m = cfg.m != 0 ? cfg.m : default_strip_width(cfg.tier);
+    if (m != 4 && m != 8 && m != 16)
+        throw std::invalid_argument("dense_gemm: strip width must be 4, 8 or 16");
+    float *dw = nullptr, *da = nullptr, *db = nullptr, *dout = nullptr;
+    auto cleanup = [&] {
+        cudaFree(dw);
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dout);
+    };
+    auto ck = [&](cudaError_t e) {
+        if (e != cudaSuccess) {
+            cleanup();
+            throw DeviceError(std::string("dense_gemm: ") + cudaGetErrorString(e));
+        }
+    };
+    ck(cudaMalloc(&dw, std::max<size_t>(w.data.size(), 1) * 4));
+    ck(cudaMalloc(&da, act.data.size() * 4));
+    ck(cudaMalloc(&dout, out.data.size() * 4));
+    if (!bias.empty()) ck(cudaMalloc(&db, bias.size() * 4));
+    ck(cudaMemcpy(dw, w.data.data(), w.data.size() * 4, cudaMemcpyHostToDevice));
+    ck(cudaMemcpy(da, act.data.data(), act.data.size() * 4, cudaMemcpyHostToDevice));
+    if (!bias.empty()) ck(cudaMemcpy(db, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+    const int rc = spcv_cu_dense_gemm_into(
+        dw, w.rows, w.cols, da, SPCV_LAYOUT_CHW, 1, act.channels, act.height, act.width, db,
+        bias.size(), act_kind(fused), fused.lo, fused.hi, dout, SPCV_LAYOUT_CHW, out.channels,
+        out.height, out.width, cfg.m, nullptr);
+    if (rc != SPCV_OK) {
+        const std::string msg = spcv_cu_last_error();
+        cleanup();
+        throw_status(rc, msg.c_str());
+    }
+    ck(cudaMemcpy(out.data.data(), dout, out.data.size() * 4, cudaMemcpyDeviceToHost));
+    cleanup();
+}
+
+Tensor dense_gemm_baseline(const DenseMatrix& w, const Tensor& act, std::span<const float> bias,
+                           const Activation& fused, const MicrokernelConfig& cfg) {
+    Tensor out(w.rows, act.height, act.width, Layout::CHW);
+    dense_gemm_into(w, act, bias, fused, out, cfg);
     return out;
 }
 

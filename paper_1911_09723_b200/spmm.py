@@ -395,3 +395,29 @@ def spmm_batched_into(w: DeviceBcsr, act, bias, fused: Activation, out,
         w.handle, act.data_ptr(), _capi.LAYOUT_CHW, B, K, H, W, bptr, blen, fused.kind, fused.lo,
         fused.hi, out.data_ptr(), _capi.LAYOUT_CHW, out.shape[1], out.shape[2], out.shape[3],
         cfg.m, cfg.n, _mode(cfg), sptr))
+
+
+def dense_gemm_batched_into(w, act, bias, fused: Activation, out, cfg: MicrokernelConfig | None = None,
+                            stream=None) -> None:
+    """Dense fp32 baseline (reference dense_gemm_into, kernels.cpp:345-373) on
+    torch CUDA tensors: w [M][K] row-major, act [B][K][H][W], out [B][M][H][W].
+    cuBLAS SGEMM (pedantic fp32) + fused bias/clamp epilogue; not bit-exact."""
+    import torch
+
+    cfg = cfg or MicrokernelConfig()
+    if act.dim() == 3:
+        act = act.unsqueeze(0)
+        out = out.unsqueeze(0)
+    for t in (w, act, out):
+        if t.device.type != "cuda" or t.dtype != torch.float32 or not t.is_contiguous():
+            raise DeviceError("dense_gemm_batched_into: contiguous CUDA float32 tensors required")
+    M, K = w.shape
+    B, C, H, W = act.shape
+    bptr, blen = (None, 0) if bias is None else (bias.data_ptr(), bias.numel())
+    if stream is None:
+        stream = torch.cuda.current_stream(act.device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    _raise(lib.spcv_cu_dense_gemm_into(
+        w.data_ptr(), M, K, act.data_ptr(), _capi.LAYOUT_CHW, B, C, H, W, bptr, blen, fused.kind,
+        fused.lo, fused.hi, out.data_ptr(), _capi.LAYOUT_CHW, out.shape[1], out.shape[2],
+        out.shape[3], cfg.m, sptr))

@@ -3,6 +3,7 @@
 // calls a reference user makes, served by the B200 kernel. Built and run by
 // tests/test_cpp_dropin.py on a GPU box. Prints "ok <name>" per case and exits
 // non-zero on the first failure.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -175,6 +176,19 @@ int main() {
             (void)spmm(m, act, std::vector<float>(3, 0.0f), Activation::none(), c2);
         }));
         std::puts("ok validation");
+    }
+    {  // test_kernels.cpp:216-239: dense baseline (cuBLAS here: fp32 rounding, not bit-exact)
+        std::mt19937 rng(43);
+        const DenseMatrix w = random_matrix(16, 16, rng);
+        const Tensor act = random_chw(16, 6, 6, rng);
+        const std::vector<float> bias = random_bias(16, rng);
+        const Tensor d = dense_gemm_baseline(w, act, bias, Activation::relu6());
+        const std::vector<float> want = dense_ref(w, act, bias, Activation::relu6());
+        double dev = 0.0;
+        for (std::size_t i = 0; i < want.size(); ++i)
+            dev = std::max(dev, static_cast<double>(std::fabs(d.data[i] - want[i])));
+        CHECK(dev <= 1e-5);
+        std::puts("ok dense_baseline");
     }
     {  // device-resident batch + bit-exact unpack
         std::mt19937 rng(41);

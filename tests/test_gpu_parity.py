@@ -494,3 +494,46 @@ def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, cas
     assert np.array_equal(bits(got), bits(want))
     fast = run_device(d.weights, d.act, d.bias, layer.act, strict=False)
     check_tolerance(d, fast, want)
+
+
+# ------------------------------------------------- dense fp32 baseline (§8f-1)
+@pytest.mark.parametrize("layer", [mbv1_pointwise()[0], mbv1_pointwise()[6], mbv1_pointwise()[12],
+                                   Layer("odd", 40, 24, 5, 7, sparsity=0.0)],
+                         ids=["pw1", "pw7", "pw13", "odd"])
+def test_dense_baseline_within_fp32_rounding(oracle, layer):
+    """dense_gemm_into (kernels.cpp:345-373) through cuBLAS SGEMM (pedantic
+    fp32): within the fp32 reordering bound of the dense oracle (the reference's
+    own dense kernel is bit-exact with matmul_reference; cuBLAS sums in its own
+    order, so the bound of check_tolerance applies with nnz_r = K)."""
+    import torch
+
+    d = make_layer_data(layer, 2, 31)
+    w = torch.from_numpy(d.dense).cuda()
+    a = torch.from_numpy(d.act).cuda()
+    o = torch.empty(2, layer.cout, layer.h, layer.w, device="cuda")
+    sp.dense_gemm_batched_into(w, a, torch.from_numpy(d.bias).cuda(), act_of(layer.act), o)
+    torch.cuda.synchronize()
+    want = np.stack([oracle.matmul_reference(d.dense, d.act[i].reshape(layer.cin, -1), d.bias, layer.act)
+                     for i in range(2)])
+    L = d.layer
+    W = np.abs(d.dense.astype(np.float64))
+    X = np.abs(d.act.astype(np.float64)).reshape(2, L.cin, -1)
+    A = np.abs(d.bias.astype(np.float64))[None, :, None] + np.einsum("mk,bks->bms", W, X)
+    tol = 1e-5 * max(1.0, L.cin / 64.0) * A
+    err = np.abs(o.cpu().numpy().reshape(A.shape).astype(np.float64) - want.reshape(A.shape))
+    assert np.all(err <= tol)
+
+
+def test_dense_baseline_validation_order():
+    import torch
+
+    w = torch.zeros(8, 8, device="cuda")
+    with pytest.raises(sp.ShapeError):
+        sp.dense_gemm_batched_into(w, torch.zeros(1, 9, 2, 2, device="cuda"), None, NONE,
+                                   torch.zeros(1, 8, 2, 2, device="cuda"))
+    with pytest.raises(sp.ShapeError):
+        sp.dense_gemm_batched_into(w, torch.zeros(1, 8, 2, 2, device="cuda"),
+                                   torch.zeros(3, device="cuda"), NONE, torch.zeros(1, 8, 2, 2, device="cuda"))
+    with pytest.raises(ValueError):
+        sp.dense_gemm_batched_into(w, torch.zeros(1, 8, 2, 2, device="cuda"), None, NONE,
+                                   torch.zeros(1, 8, 2, 2, device="cuda"), sp.MicrokernelConfig(m=5))
