@@ -5,7 +5,9 @@
 // reference's bench does (bench.cpp:216-227).
 #include <cublas_v2.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "spcv_internal.h"
@@ -45,7 +47,11 @@ int get_handle(cublasHandle_t* out) {
     cublasHandle_t h = nullptr;
     if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS)
         return fail(SPCV_ERR_CUDA, "dense_gemm: cublasCreate failed");
-    cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);  // strict fp32: no TF32 / reduced precision
+    // fp32 without TF32: CUBLAS_DEFAULT_MATH never uses TF32 tensor cores for
+    // SGEMM; SPCV_DENSE_MATH=pedantic additionally forbids reduced-precision
+    // internals (slower).
+    const char* m = std::getenv("SPCV_DENSE_MATH");
+    cublasSetMathMode(h, (m && std::string(m) == "pedantic") ? CUBLAS_PEDANTIC_MATH : CUBLAS_DEFAULT_MATH);
     handles.push_back({dev, h});
     *out = h;
     return SPCV_OK;

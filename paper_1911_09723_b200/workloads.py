@@ -39,6 +39,7 @@ class Layer:
     sparsity: float = 0.9
     block_h: int = 1
     skew: bool = False   # per-row Beta(2,8) densities (config 5)
+    net_index: int = -1  # index in the reference network's layer list (netdef.cpp)
 
     @property
     def spatial(self) -> int:
@@ -49,7 +50,8 @@ def mbv1_pointwise(sparsity: float = 0.9) -> list[Layer]:
     """MBv1-1.0 @224: the 13 pointwise layers (netdef.cpp:205-211)."""
     shapes = [(32, 64, 112), (64, 128, 56), (128, 128, 56), (128, 256, 28), (256, 256, 28),
               (256, 512, 14)] + [(512, 512, 14)] * 5 + [(512, 1024, 7), (1024, 1024, 7)]
-    return [Layer(f"pw{i + 1}", k, m, hw, hw, RELU6, 0.0, 6.0, sparsity)
+    # layer list: entry conv (0), then dw_i (2i-1), pw_i (2i) for i = 1..13
+    return [Layer(f"pw{i + 1}", k, m, hw, hw, RELU6, 0.0, 6.0, sparsity, net_index=2 * (i + 1))
             for i, (k, m, hw) in enumerate(shapes)]
 
 
@@ -60,18 +62,23 @@ def mbv2_pointwise(sparsity: float = 0.85) -> list[Layer]:
     stages = [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1),
               (6, 160, 3, 2), (6, 320, 1, 1)]
     layers: list[Layer] = []
-    c, hw, blk = 32, 112, 0
+    c, hw, blk, idx = 32, 112, 0, 1  # layer 0 is the entry conv (netdef.cpp:176)
     for t, cout, n, s in stages:
         for i in range(n):
             blk += 1
             stride = s if i == 0 else 1
             if t != 1:
-                layers.append(Layer(f"b{blk}_expand", c, c * t, hw, hw, RELU6, -1.0, 1.0, sparsity))
+                layers.append(Layer(f"b{blk}_expand", c, c * t, hw, hw, RELU6, -1.0, 1.0, sparsity,
+                                    net_index=idx))
+                idx += 1
             hidden = c * t
             hw = (hw + stride - 1) // stride
-            layers.append(Layer(f"b{blk}_project", hidden, cout, hw, hw, NONE, 0.0, 6.0, sparsity))
+            idx += 1  # depthwise
+            layers.append(Layer(f"b{blk}_project", hidden, cout, hw, hw, NONE, 0.0, 6.0, sparsity,
+                                net_index=idx))
+            idx += 1
             c = cout
-    layers.append(Layer("head", c, 1280, hw, hw, RELU6, -1.0, 1.0, sparsity))
+    layers.append(Layer("head", c, 1280, hw, hw, RELU6, -1.0, 1.0, sparsity, net_index=idx))
     return layers
 
 

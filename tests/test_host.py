@@ -208,3 +208,31 @@ def test_skewed_rows_mean_density():
 def test_uniform_mask_exact_count():
     d = make_layer_data(mbv1_pointwise()[0], 1, 1, act=False)
     assert d.weights.nnz_values() == 2048 - int(np.floor(2048 * 0.9 + 0.5))
+
+
+def test_bench_layers_csv_schema_matches_reference():
+    """tools/bench_layers.py emits the reference's 11-column schema
+    (bench.cpp:428-445) with %.17g doubles."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "bench_layers", os.path.join(ROOT, "tools", "bench_layers.py"))
+    bl = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bl)
+    assert bl.CSV_HEADER == ("layer_index,kind,cout,cin,spatial,sparsity,block_h,variant,median_ns,"
+                             "achieved_gflops,effective_gflops")
+    text = bl.rows_to_csv([dict(layer_index=2, kind="pointwise", cout=64, cin=32, spatial=12544,
+                                sparsity=0.9, block_h=1, variant="b200-strict", median_ns=1234.5,
+                                achieved_gflops=0.1, effective_gflops=1.0 / 3.0)])
+    lines = text.strip().split("\n")
+    assert lines[0] == bl.CSV_HEADER
+    assert lines[1] == "2,pointwise,64,32,12544,0.90000000000000002,1,b200-strict,1234.5,0.10000000000000001,0.33333333333333331"
+
+
+def test_network_layer_indices():
+    v1 = mbv1_pointwise()
+    assert [l.net_index for l in v1] == [2 * i for i in range(1, 14)]
+    v2 = mbv2_pointwise()
+    assert v2[0].name == "b1_project" and v2[0].net_index == 2  # entry, dw, project
+    assert v2[1].name == "b2_expand" and v2[1].net_index == 3
+    assert v2[-1].name == "head" and v2[-1].net_index == 51  # 16 expands + 17 (dw, project) + entry
