@@ -105,6 +105,19 @@ int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_l
                            int out_layout, int out_c, int out_h, int out_w, int cfg_m, int cfg_n,
                            int mode);
 
+/* The network executor's pointwise step (run_network, netdef.cpp:494-512) on
+ * device tensors, fused: weights may carry padded rows (w.rows > out_c, up to
+ * block_h-1 extra rows; they are computed with bias 0 and never stored, i.e.
+ * the "run wide, keep the logical prefix" of netdef.cpp:496-505), and an
+ * optional residual [images][out_c][H*W] is added after the activation
+ * (add_residual, netdef.cpp:448-452,512: out = act(acc) + res, separately
+ * rounded). bias has out_c entries or none. act [images][act_c][H*W], out
+ * [images][out_c][H*W]. Same arithmetic modes as spcv_cu_spmm_into. */
+int spcv_cu_spmm_layer(const spcv_cu_weights* w, const float* act, int images, int act_c,
+                       int act_h, int act_w, const float* bias, size_t bias_len, int act_kind,
+                       float lo, float hi, const float* residual, float* out, int out_c, int mode,
+                       void* stream);
+
 /* Dense fp32 baseline with the same contract as the SpMM entry point: the
  * reference's dense_gemm_into (kernels.hpp:85-90, kernels.cpp:345-373), its
  * in-repo speed baseline for the sparse kernel (bench.cpp:216-227). `w` is a

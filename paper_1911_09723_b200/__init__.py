@@ -29,6 +29,7 @@ from .spmm import (
     spmm_batched_into,
     spmm_host_batched,
     spmm_into,
+    spmm_layer,
     variant_name,
 )
 
@@ -36,6 +37,6 @@ __all__ = [
     "Activation", "BcsrMatrix", "dense_gemm_batched_into", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
     "LayoutError", "MicrokernelConfig", "ShapeError", "Tensor", "Tier", "decode_bcsr",
     "default_strip_width", "encode_bcsr", "parse_tier", "parse_variant", "resolve_tier",
-    "spconv_1x1", "spmm", "spmm_batched_into", "spmm_host_batched", "spmm_into",
+    "spconv_1x1", "spmm", "spmm_batched_into", "spmm_host_batched", "spmm_into", "spmm_layer",
     "variant_name", "launch_count", "LIB_PATH",
 ]

@@ -28,6 +28,7 @@ SIGNATURES = {
     "spcv_cu_free": (None, [_p]),
     "spcv_cu_spmm_into": (_i, _SPMM_ARGS + [_p]),
     "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
+    "spcv_cu_spmm_layer": (_i, [_p, _p, _i, _i, _i, _i, _p, _z, _i, _f, _f, _p, _p, _i, _i, _p]),
     "spcv_cu_dense_gemm_into": (_i, [_p, _i, _i] + _SPMM_ARGS[1:17] + [_i, _p]),
     "spcv_cu_launch_count": (_u64, []),
     "spcv_cu_last_error": (ctypes.c_char_p, []),

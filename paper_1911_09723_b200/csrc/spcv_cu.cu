@@ -409,7 +409,7 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
 
 int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, int act_w,
            const float* bias, int act_kind, float lo, float hi, float* out, int mode,
-           cudaStream_t st) {
+           cudaStream_t st, int out_rows = -1, const float* residual = nullptr) {
     const long long S = static_cast<long long>(act_h) * act_w;
     const long long N = S * images;
     if (N == 0) return SPCV_OK;
@@ -430,6 +430,8 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.N = N;
     a.K = w->cols;
     a.M = w->rows;
+    a.M_out = out_rows < 0 ? w->rows : out_rows;
+    a.residual = residual;
     a.S = static_cast<int>(S);
     a.act_kind = act_kind;
     a.lo = lo;
@@ -440,7 +442,8 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
     const int sms = props_for(dev).sms;
     const bool vec = (S % 4 == 0) && (reinterpret_cast<uintptr_t>(act) % 16 == 0) &&
-                     (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(residual) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
     switch (w->block_h) {
         case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);
@@ -488,6 +491,34 @@ extern "C" int spcv_cu_spmm_into(const spcv_cu_weights* w, const float* act, int
     if (rc) return rc;
     return launch(w, act, images, act_h, act_w, bias_len ? bias : nullptr, act_kind, lo, hi, out,
                   mode, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int spcv_cu_spmm_layer(const spcv_cu_weights* w, const float* act, int images,
+                                  int act_c, int act_h, int act_w, const float* bias,
+                                  size_t bias_len, int act_kind, float lo, float hi,
+                                  const float* residual, float* out, int out_c, int mode,
+                                  void* stream) {
+    g_last_error.clear();
+    if (!w) return fail(SPCV_ERR_INVALID, "spmm_layer: null weights");
+    if (act_kind != SPCV_ACT_NONE && act_kind != SPCV_ACT_CLAMP)
+        return fail(SPCV_ERR_INVALID, "spmm_layer: unknown activation kind");
+    if (act_kind == SPCV_ACT_CLAMP && !(lo < hi)) return fail(SPCV_ERR_INVALID, "clamp requires lo < hi");
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "spmm_layer: unknown arithmetic mode");
+    if (w->cols != act_c)
+        return fail(SPCV_ERR_SHAPE, "spmm_layer: weight cols " + std::to_string(w->cols) +
+                                        " != activation channels " + std::to_string(act_c));
+    // padded rows: the stored weights may have up to block_h-1 rows beyond
+    // the layer's logical output channels (netdef.cpp:496-505)
+    if (out_c < 1 || out_c > w->rows || w->rows - out_c >= w->block_h)
+        return fail(SPCV_ERR_SHAPE, "spmm_layer: out channels " + std::to_string(out_c) +
+                                        " incompatible with " + std::to_string(w->rows) +
+                                        " weight rows of block height " + std::to_string(w->block_h));
+    if (bias_len != 0 && bias_len != static_cast<size_t>(out_c))
+        return fail(SPCV_ERR_SHAPE, "spmm_layer: bias length != out channels");
+    if (images < 0 || act_h < 1 || act_w < 1) return fail(SPCV_ERR_SHAPE, "spmm_layer: bad dims");
+    return launch(w, act, images, act_h, act_w, bias_len ? bias : nullptr, act_kind, lo, hi, out, mode,
+                  static_cast<cudaStream_t>(stream), out_c, residual);
 }
 
 extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_layout,

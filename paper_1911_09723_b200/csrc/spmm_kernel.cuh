@@ -56,7 +56,9 @@ struct KernelArgs {
     const uint4* stream;     // chunk stream (chunk_bytes_g<BH,STEPS>(G) bytes per chunk)
     const uint32_t* bin_beg; // kBins + 1 chunk offsets
     long long N;             // images * S
-    int K, M, S;
+    int K, M, S;             // M: weight rows (block rows * block_h)
+    int M_out;               // rows stored (<= M): the executor's padded-row truncation
+    const float* residual;   // nullptr or [images][M_out][S], added after the activation
     int act_kind;            // 0 none, 1 clamp
     float lo, hi;
     // Tail splitting (kernel 1): CTAs blockIdx.x >= tail_start share their
@@ -153,7 +155,7 @@ struct Chunk {
 __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a) {
     if (n >= a.N) return -1;
     const long long b = n / a.S;
-    return b * static_cast<long long>(a.M) * a.S + (n - b * a.S);
+    return b * static_cast<long long>(a.M_out) * a.S + (n - b * a.S);
 }
 
 #ifndef SPCV_HOIST
@@ -211,7 +213,9 @@ struct Exec {
             const int col = static_cast<int>(lane_off[j] >> 2);  // first column of the quad
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
-                const long long roff = (static_cast<long long>(brow) * BH + i) * a.S;
+                const int r = static_cast<int>(brow) * BH + i;
+                if (r >= a.M_out) continue;  // padded row: computed, never stored (netdef.cpp:496-505)
+                const long long roff = static_cast<long long>(r) * a.S;
                 float4 v = acc[i][j];
                 v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
                 v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
@@ -219,13 +223,26 @@ struct Exec {
                 v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
                 if constexpr (VEC) {
                     const long long o = ocol[j];
-                    if (o >= 0) __stcs(reinterpret_cast<float4*>(a.out + o + roff), v);
+                    if (o >= 0) {
+                        if (a.residual != nullptr) {  // out = act(acc) + res (netdef.cpp:448-452,512)
+                            const float4 rv = __ldcs(reinterpret_cast<const float4*>(a.residual + o + roff));
+                            v.x = __fadd_rn(v.x, rv.x);
+                            v.y = __fadd_rn(v.y, rv.y);
+                            v.z = __fadd_rn(v.z, rv.z);
+                            v.w = __fadd_rn(v.w, rv.w);
+                        }
+                        __stcs(reinterpret_cast<float4*>(a.out + o + roff), v);
+                    }
                 } else {
                     const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const long long o = s_col[col + q];
-                        if (o >= 0) __stcs(a.out + o + roff, e[q]);
+                        if (o >= 0) {
+                            float x = e[q];
+                            if (a.residual != nullptr) x = __fadd_rn(x, __ldcs(a.residual + o + roff));
+                            __stcs(a.out + o + roff, x);
+                        }
                     }
                 }
             }
@@ -394,8 +411,10 @@ spmm_bcsr_kernel(const KernelArgs a) {
     const long long n0 = tile * T;
 
     // ---- stage bias, zero row, column offsets and the [K][T] activation tile ----
-    if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += nthreads) cp_async4(s_bias + i, a.bias + i);
+    if (a.bias != nullptr) {  // logical rows from bias; padded rows (never stored) get 0
+        for (int i = tid; i < a.M_out; i += nthreads) cp_async4(s_bias + i, a.bias + i);
+        for (int i = a.M_out + tid; i < a.M; i += nthreads) s_bias[i] = 0.0f;
+    }
     for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
         reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
             make_float4(0.f, 0.f, 0.f, 0.f);
@@ -524,7 +543,7 @@ spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += blockDim.x) s_bias[i] = __ldg(a.bias + i);
+        for (int i = tid; i < a.M; i += blockDim.x) s_bias[i] = i < a.M_out ? __ldg(a.bias + i) : 0.0f;
     for (int s = 0; s < nstages; ++s) {  // zero rows (never overwritten by copies)
         float* zr = reinterpret_cast<float*>(stages + s * stage_bytes) + static_cast<size_t>(a.K) * T;
         for (int i = tid; i < T; i += blockDim.x) zr[i] = 0.f;

@@ -421,3 +421,33 @@ def dense_gemm_batched_into(w, act, bias, fused: Activation, out, cfg: Microkern
         w.data_ptr(), M, K, act.data_ptr(), _capi.LAYOUT_CHW, B, C, H, W, bptr, blen, fused.kind,
         fused.lo, fused.hi, out.data_ptr(), _capi.LAYOUT_CHW, out.shape[1], out.shape[2],
         out.shape[3], cfg.m, sptr))
+
+
+def spmm_layer(w: DeviceBcsr, act, bias, fused: Activation, out, residual=None,
+               strict: bool = True, stream=None) -> None:
+    """The executor's pointwise step on device (run_network, netdef.cpp:494-512):
+    `w` may carry padded rows (rows padded to the block height); only the
+    first out.shape[1] rows are stored. `residual` (optional, out's shape) is
+    added after the activation (add_residual, netdef.cpp:448-452)."""
+    import torch
+
+    if act.dim() == 3:
+        act = act.unsqueeze(0)
+        out = out.unsqueeze(0)
+        residual = None if residual is None else residual.unsqueeze(0)
+    for t in (act, out) + (() if residual is None else (residual,)):
+        if t.device.type != "cuda" or t.dtype != torch.float32 or not t.is_contiguous():
+            raise DeviceError("spmm_layer: contiguous CUDA float32 tensors required")
+    if residual is not None and tuple(residual.shape) != tuple(out.shape):
+        raise ShapeError("spmm_layer: residual shape != output shape")
+    B, K, H, W = act.shape
+    if tuple(out.shape) != (B, out.shape[1], H, W):
+        raise ShapeError("spmm_layer: output shape mismatch")
+    bptr, blen = (None, 0) if bias is None else (bias.data_ptr(), bias.numel())
+    if stream is None:
+        stream = torch.cuda.current_stream(act.device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    _raise(lib.spcv_cu_spmm_layer(
+        w.handle, act.data_ptr(), B, K, H, W, bptr, blen, fused.kind, fused.lo, fused.hi,
+        None if residual is None else residual.data_ptr(), out.data_ptr(), out.shape[1],
+        _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))

@@ -537,3 +537,54 @@ def test_dense_baseline_validation_order():
     with pytest.raises(ValueError):
         sp.dense_gemm_batched_into(w, torch.zeros(1, 8, 2, 2, device="cuda"), None, NONE,
                                    torch.zeros(1, 8, 2, 2, device="cuda"), sp.MicrokernelConfig(m=5))
+
+
+# ------------------------------- executor pointwise step on device (§8f-2)
+@pytest.mark.parametrize("hw", [(7, 9), (8, 8)], ids=["odd_spatial", "vec"])
+@pytest.mark.parametrize("bh", [2, 4])
+def test_spmm_layer_padded_rows_and_residual(oracle, hw, bh):
+    """run_network's pointwise branch (netdef.cpp:494-512): weights padded to
+    the block height are run wide (pad rows bias 0) and truncated to the
+    logical rows; the residual is added after the activation. Bit-exact
+    against the oracle doing the same steps on the host."""
+    import torch
+
+    H, W = hw
+    rows, K, B = 10, 24, 3
+    rng = np.random.default_rng(5)
+    dense = (rng.standard_normal((rows, K)) * 0.3).astype(np.float32)
+    dense[rng.random((rows, K)) < 0.6] = 0
+    pad = (-rows) % bh
+    wide = np.vstack([dense, np.zeros((pad, K), np.float32)])
+    m = sp.encode_bcsr(wide, bh)
+    act = rng.uniform(-1, 1, (B, K, H, W)).astype(np.float32)
+    bias = rng.uniform(-1, 1, rows).astype(np.float32)
+    res = rng.uniform(-1, 1, (B, rows, H, W)).astype(np.float32)
+    want = oracle.spmm(m, act, np.r_[bias, np.zeros(pad, np.float32)], RELU6)[:, :rows].reshape(B, rows, H, W)
+    want_res = (want + res).astype(np.float32)
+    dw = sp.DeviceBcsr(m)
+    a = torch.from_numpy(act).cuda()
+    o = torch.full((B, rows, H, W), float("nan"), device="cuda")
+    sp.spmm_layer(dw, a, torch.from_numpy(bias).cuda(), RELU6, o)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o.cpu().numpy()), bits(want))
+    sp.spmm_layer(dw, a, torch.from_numpy(bias).cuda(), RELU6, o, residual=torch.from_numpy(res).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o.cpu().numpy()), bits(want_res))
+
+
+def test_spmm_layer_checks():
+    import torch
+
+    m = sp.encode_bcsr(np.ones((12, 8), np.float32), 4)
+    dw = sp.DeviceBcsr(m)
+    a = torch.zeros(1, 8, 2, 2, device="cuda")
+    with pytest.raises(sp.ShapeError):  # more logical rows than stored
+        sp.spmm_layer(dw, a, None, NONE, torch.zeros(1, 13, 2, 2, device="cuda"))
+    with pytest.raises(sp.ShapeError):  # padding larger than one block
+        sp.spmm_layer(dw, a, None, NONE, torch.zeros(1, 8, 2, 2, device="cuda"))
+    with pytest.raises(sp.ShapeError):  # bias must match the logical rows
+        sp.spmm_layer(dw, a, torch.zeros(12, device="cuda"), NONE, torch.zeros(1, 10, 2, 2, device="cuda"))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_layer(dw, torch.zeros(1, 9, 2, 2, device="cuda"), None, NONE,
+                      torch.zeros(1, 10, 2, 2, device="cuda"))
