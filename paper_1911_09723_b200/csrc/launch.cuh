@@ -26,10 +26,10 @@ struct Geometry {
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
-int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
-               cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC>;
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES>
+int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
+                 cudaStream_t st) {
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -56,6 +56,15 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
     SPCV_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
+}
+
+// Residual-add epilogue as a separate instantiation (the plain path keeps
+// its register budget).
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
+int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
+               cudaStream_t st) {
+    return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true>(a, w, ntiles, sms, st)
+                      : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
 }
 
 // Shared memory of the pipelined kernel with `ns` stages.

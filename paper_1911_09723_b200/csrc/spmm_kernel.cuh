@@ -163,7 +163,7 @@ __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a
 #endif
 constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of their FMAs
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES = false>
 struct Exec {
     static constexpr int G = 32 / LPR;
     static constexpr int T = LPR * NF * 4;
@@ -224,7 +224,7 @@ struct Exec {
                 if constexpr (VEC) {
                     const long long o = ocol[j];
                     if (o >= 0) {
-                        if (a.residual != nullptr) {  // out = act(acc) + res (netdef.cpp:448-452,512)
+                        if constexpr (RES) {  // out = act(acc) + res (netdef.cpp:448-452,512)
                             const float4 rv = __ldcs(reinterpret_cast<const float4*>(a.residual + o + roff));
                             v.x = __fadd_rn(v.x, rv.x);
                             v.y = __fadd_rn(v.y, rv.y);
@@ -240,7 +240,7 @@ struct Exec {
                         const long long o = s_col[col + q];
                         if (o >= 0) {
                             float x = e[q];
-                            if (a.residual != nullptr) x = __fadd_rn(x, __ldcs(a.residual + o + roff));
+                            if constexpr (RES) x = __fadd_rn(x, __ldcs(a.residual + o + roff));
                             __stcs(a.out + o + roff, x);
                         }
                     }
@@ -384,10 +384,10 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
 
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 spmm_bcsr_kernel(const KernelArgs a) {
-    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC>;
+    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES>;
     constexpr int G = E::G;
     constexpr int T = E::T;
     constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
