@@ -38,7 +38,14 @@ typedef enum spcv_status {
     SPCV_ERR_FORMAT = 3,   /* spcv::FormatError      (sparse.hpp:12-15)   */
     SPCV_ERR_INVALID = 4,  /* std::invalid_argument  (kernels.cpp:321-322) */
     SPCV_ERR_CUDA = 5,     /* CUDA runtime failure (no device, launch error, ...) */
-    SPCV_ERR_UNSUPPORTED = 6 /* shape beyond this build's device limits */
+    SPCV_ERR_UNSUPPORTED = 6, /* shape beyond this build's device limits */
+    /* model files (model_io.hpp:13-46) */
+    SPCV_ERR_MODEL_IO = 7,     /* spcv::ModelIoError (generic)                 */
+    SPCV_ERR_BAD_MAGIC = 8,    /* spcv::BadMagicError                          */
+    SPCV_ERR_VERSION = 9,      /* spcv::UnsupportedVersionError                */
+    SPCV_ERR_TRUNCATED = 10,   /* spcv::TruncatedError                         */
+    SPCV_ERR_CHECKSUM = 11,    /* spcv::ChecksumError                          */
+    SPCV_ERR_MODEL_FORMAT = 12 /* spcv::ModelFormatError                       */
 } spcv_status;
 
 /* Tensor layouts, as spcv::Layout (tensor.hpp:23-26). */
@@ -131,6 +138,37 @@ int spcv_cu_dense_gemm_into(const float* w, int rows, int cols, const float* act
                             size_t bias_len, int act_kind, float lo, float hi, float* out,
                             int out_layout, int out_c, int out_h, int out_w, int cfg_m,
                             void* stream);
+
+/* ---- SPCV model files -------------------------------------
+ * The reference's model container ("SPCV" magic, u16 version 1, network
+ * descriptor, layer records, CRC-32 trailer; model_io.hpp:48-55) parsed with
+ * parse_model's checks in its order (model_io.cpp:238-381) and its typed
+ * errors (SPCV_ERR_BAD_MAGIC ... SPCV_ERR_MODEL_FORMAT). */
+typedef struct spcv_cu_model spcv_cu_model;
+
+/* Parse and fully validate without touching the device; *layers = count. */
+int spcv_cu_model_parse(const uint8_t* bytes, size_t size, int* layers);
+
+/* Parse, then upload once: every sparse 1x1 / classifier layer is packed
+ * (spcv_cu_pack) with its bias; dense ones are uploaded row-major. */
+int spcv_cu_model_load(const uint8_t* bytes, size_t size, spcv_cu_model** out);
+
+/* Layer i: info[12] = {kind (0 entry, 1 pointwise, 2 depthwise, 3 pool,
+ * 4 classifier), cin, cout, in_h, in_w, out_h, out_w, is_sparse, block_h,
+ * act_kind, residual_src, stride}. */
+int spcv_cu_model_layer(const spcv_cu_model* m, int i, int* info);
+
+/* Borrowed packed weights of sparse layer i (owned by the model). */
+int spcv_cu_model_weights(const spcv_cu_model* m, int i, const spcv_cu_weights** w);
+
+/* Run 1x1 / classifier layer i as run_network's pointwise step
+ * (netdef.cpp:494-512): its bias, fused activation, padded-row truncation,
+ * and the residual (device [images][cout][out_h*out_w], required iff the
+ * layer has a residual source). act [images][cin][in_h*in_w] on device. */
+int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act, int images,
+                      const float* residual, float* out, int mode, void* stream);
+
+void spcv_cu_model_free(spcv_cu_model* m);
 
 /* Number of SpMM kernel launches issued by this library so far (process-wide). */
 uint64_t spcv_cu_launch_count(void);

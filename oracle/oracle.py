@@ -135,6 +135,10 @@ class Ref:
         lib.ref_encode_bcsr.argtypes = [_i, _i, _i, _p, _p, _p, _p, ctypes.POINTER(_z)]
         lib.ref_validate_bcsr.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z]
         lib.ref_generate_mask.argtypes = [_i, _i, _d, _i, _i, ctypes.c_uint32, _p]
+        lib.ref_model_bytes.argtypes = [ctypes.c_char_p, _d, _d, ctypes.c_uint32, _p, _z,
+                                        ctypes.POINTER(_z)]
+        lib.ref_model_parse.argtypes = [_p, _z, ctypes.POINTER(_i)]
+        lib.ref_model_layer.argtypes = [_p, _z, _i, _p, _p, _p, _p, _p]
         lib.ref_bench_layers.argtypes = [ctypes.POINTER(RefLayer), _i, _i, _i, _i, ctypes.POINTER(_d)]
         lib.ref_bench_spmm.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z, _i, _i, _i, _p, _p, _i,
                                        _f, _f, _p, _i, _i, _i, ctypes.POINTER(_d)]
@@ -212,6 +216,43 @@ class Ref:
         assert rc == 0, rc
         return [secs[i] for i in range(reps)]
 
+
+    def model_bytes(self, arch: str, width: float, sparsity: float, seed: int) -> bytes:
+        """serialize_model(build_network(arch, width, default_plan(arch, sparsity)),
+        instantiate_weights(seed)) — a reference model file."""
+        n = _z(0)
+        rc = self.lib.ref_model_bytes(arch.encode(), width, sparsity, seed, None, 0, ctypes.byref(n))
+        assert rc == 0, rc
+        buf = np.zeros(n.value, np.uint8)
+        rc = self.lib.ref_model_bytes(arch.encode(), width, sparsity, seed, buf.ctypes.data, buf.size,
+                                      ctypes.byref(n))
+        assert rc == 0, rc
+        return buf.tobytes()
+
+    def model_parse(self, data: bytes):
+        """parse_model: (status code, layer count)."""
+        buf = np.frombuffer(data, np.uint8)
+        layers = _i(0)
+        rc = self.lib.ref_model_parse(buf.ctypes.data if buf.size else None, buf.size, ctypes.byref(layers))
+        return rc, layers.value
+
+    def model_layer(self, data: bytes, i: int):
+        """Layer i of parse_model: meta dict and (row_ptr, col_idx, values, bias)."""
+        buf = np.frombuffer(data, np.uint8)
+        meta = np.zeros(12, np.int32)
+        rc = self.lib.ref_model_layer(buf.ctypes.data, buf.size, i, meta.ctypes.data, None, None, None, None)
+        assert rc == 0, rc
+        names = ["kind", "cin", "cout", "is_sparse", "rows", "cols", "block_h", "nrp", "nblk", "nval",
+                 "nbias", "residual_src"]
+        m = dict(zip(names, meta.tolist()))
+        rp = np.zeros(max(m["nrp"], 1), np.uint32)
+        ci = np.zeros(max(m["nblk"], 1), np.uint32)
+        va = np.zeros(max(m["nval"], 1), np.float32)
+        bi = np.zeros(max(m["nbias"], 1), np.float32)
+        rc = self.lib.ref_model_layer(buf.ctypes.data, buf.size, i, meta.ctypes.data, rp.ctypes.data,
+                                      ci.ctypes.data, va.ctypes.data, bi.ctypes.data)
+        assert rc == 0, rc
+        return m, (rp[:m["nrp"]], ci[:m["nblk"]], va[:m["nval"]], bi[:m["nbias"]])
 
     def bench_layers(self, layers, nthreads, warmups=0, reps=1):
         """Timed reference spmm_into over several layers' (weights, act [B][K][H][W],

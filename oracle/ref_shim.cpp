@@ -21,6 +21,8 @@
 #include <vector>
 
 #include "spcv/kernels.hpp"
+#include "spcv/model_io.hpp"
+#include "spcv/netdef.hpp"
 #include "spcv/sparse.hpp"
 #include "spcv/tensor.hpp"
 
@@ -29,6 +31,18 @@ namespace {
 int code_of(const std::exception_ptr& e) {
     try {
         std::rethrow_exception(e);
+    } catch (const spcv::BadMagicError&) {
+        return 8;
+    } catch (const spcv::UnsupportedVersionError&) {
+        return 9;
+    } catch (const spcv::TruncatedError&) {
+        return 10;
+    } catch (const spcv::ChecksumError&) {
+        return 11;
+    } catch (const spcv::ModelFormatError&) {
+        return 12;
+    } catch (const spcv::ModelIoError&) {
+        return 7;
     } catch (const spcv::LayoutError&) {
         return 1;
     } catch (const spcv::ShapeError&) {
@@ -284,6 +298,62 @@ int ref_bench_layers(const RefLayer* L, int nlayers, int nthreads, int warmups, 
             pass();
             secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// ---------------------------------------------------------------- model files
+// serialize_model(build_network(arch, width, default_plan(arch, sparsity)),
+// instantiate_weights(seed)) (model_io.cpp:146-227, netdef.cpp:234-404).
+// Two-call: with buf == null (or too small) only *n is written.
+int ref_model_bytes(const char* arch, double width, double sparsity, std::uint32_t seed,
+                    std::uint8_t* buf, std::size_t cap, std::size_t* n) {
+    try {
+        const spcv::NetworkSpec net =
+            spcv::build_network(arch, width, spcv::default_plan(arch, sparsity));
+        const spcv::WeightSet ws = spcv::instantiate_weights(net, seed);
+        const std::vector<std::uint8_t> bytes = spcv::serialize_model(net, ws);
+        *n = bytes.size();
+        if (buf && cap >= bytes.size()) std::memcpy(buf, bytes.data(), bytes.size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// parse_model (model_io.cpp:238-381): 0 or the typed-error code.
+int ref_model_parse(const std::uint8_t* data, std::size_t size, int* layers) {
+    try {
+        const auto parsed = spcv::parse_model(data, size);
+        if (layers) *layers = static_cast<int>(parsed.first.layers.size());
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// Layer i of a parsed model: kind, cout, storage and (two-call) the BCSR
+// arrays of a sparse layer. meta = {kind, cin, cout, is_sparse, rows, cols,
+// block_h, nrp, nblk, nval, nbias, residual_src}.
+int ref_model_layer(const std::uint8_t* data, std::size_t size, int i, int* meta,
+                    std::uint32_t* row_ptr, std::uint32_t* col_idx, float* values, float* bias) {
+    try {
+        const auto parsed = spcv::parse_model(data, size);
+        const spcv::LayerSpec& L = parsed.first.layers.at(static_cast<std::size_t>(i));
+        const spcv::LayerWeights& w = parsed.second.layers.at(static_cast<std::size_t>(i));
+        const int m[12] = {static_cast<int>(L.kind), L.cin, L.cout, w.is_sparse ? 1 : 0,
+                           w.sparse.rows, w.sparse.cols, w.sparse.block_h,
+                           static_cast<int>(w.sparse.row_ptr.size()),
+                           static_cast<int>(w.sparse.col_idx.size()),
+                           static_cast<int>(w.sparse.values.size()),
+                           static_cast<int>(w.bias.size()), L.residual_src};
+        std::copy(m, m + 12, meta);
+        if (row_ptr) std::copy(w.sparse.row_ptr.begin(), w.sparse.row_ptr.end(), row_ptr);
+        if (col_idx) std::copy(w.sparse.col_idx.begin(), w.sparse.col_idx.end(), col_idx);
+        if (values) std::copy(w.sparse.values.begin(), w.sparse.values.end(), values);
+        if (bias) std::copy(w.bias.begin(), w.bias.end(), bias);
         return 0;
     } catch (...) {
         return code_of(std::current_exception());

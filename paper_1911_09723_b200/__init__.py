@@ -6,6 +6,14 @@ kernels behind the C-ABI in ``include/spcv_cu.h``. See DESIGN.md.
 """
 from ._capi import LIB_PATH, launch_count
 from .spmm import (
+    BadMagicError,
+    ChecksumError,
+    DeviceModel,
+    ModelFormatError,
+    ModelIoError,
+    TruncatedError,
+    UnsupportedVersionError,
+    parse_model_status,
     Activation,
     BcsrMatrix,
     DeviceBcsr,
@@ -34,6 +42,8 @@ from .spmm import (
 )
 
 __all__ = [
+    "BadMagicError", "ChecksumError", "DeviceModel", "ModelFormatError", "ModelIoError",
+    "TruncatedError", "UnsupportedVersionError", "parse_model_status",
     "Activation", "BcsrMatrix", "dense_gemm_batched_into", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
     "LayoutError", "MicrokernelConfig", "ShapeError", "Tensor", "Tier", "decode_bcsr",
     "default_strip_width", "encode_bcsr", "parse_tier", "parse_variant", "resolve_tier",

@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("SPCV_CU_LIB") or os.path.join(LIB_DIR, "libspcv_cu.so
 
 # spcv_status (include/spcv_cu.h)
 OK, ERR_LAYOUT, ERR_SHAPE, ERR_FORMAT, ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+ERR_MODEL_IO, ERR_BAD_MAGIC, ERR_VERSION, ERR_TRUNCATED, ERR_CHECKSUM, ERR_MODEL_FORMAT = range(7, 13)
 LAYOUT_CHW, LAYOUT_HWC = 0, 1
 ACT_NONE, ACT_CLAMP = 0, 1
 MODE_STRICT, MODE_FAST = 0, 1
@@ -30,6 +31,12 @@ SIGNATURES = {
     "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
     "spcv_cu_spmm_layer": (_i, [_p, _p, _i, _i, _i, _i, _p, _z, _i, _f, _f, _p, _p, _i, _i, _p]),
     "spcv_cu_dense_gemm_into": (_i, [_p, _i, _i] + _SPMM_ARGS[1:17] + [_i, _p]),
+    "spcv_cu_model_parse": (_i, [_p, _z, _p]),
+    "spcv_cu_model_load": (_i, [_p, _z, ctypes.POINTER(_p)]),
+    "spcv_cu_model_layer": (_i, [_p, _i, _p]),
+    "spcv_cu_model_weights": (_i, [_p, _i, ctypes.POINTER(_p)]),
+    "spcv_cu_model_run": (_i, [_p, _i, _p, _i, _p, _p, _i, _p]),
+    "spcv_cu_model_free": (None, [_p]),
     "spcv_cu_launch_count": (_u64, []),
     "spcv_cu_last_error": (ctypes.c_char_p, []),
     "spcv_cu_version": (ctypes.c_char_p, []),

@@ -44,6 +44,30 @@ class DeviceError(RuntimeError):
     """CUDA failure or a shape beyond the device limits (no reference counterpart)."""
 
 
+class ModelIoError(RuntimeError):
+    """model_io.hpp:13-16 and its subclasses below (model_io.hpp:18-46)."""
+
+
+class BadMagicError(ModelIoError):
+    pass
+
+
+class UnsupportedVersionError(ModelIoError):
+    pass
+
+
+class TruncatedError(ModelIoError):
+    pass
+
+
+class ChecksumError(ModelIoError):
+    pass
+
+
+class ModelFormatError(ModelIoError):
+    pass
+
+
 def _raise(status: int) -> None:
     if status == _capi.OK:
         return
@@ -56,6 +80,11 @@ def _raise(status: int) -> None:
         raise FormatError(msg)
     if status == _capi.ERR_INVALID:
         raise ValueError(msg)
+    model_errors = {_capi.ERR_MODEL_IO: ModelIoError, _capi.ERR_BAD_MAGIC: BadMagicError,
+                    _capi.ERR_VERSION: UnsupportedVersionError, _capi.ERR_TRUNCATED: TruncatedError,
+                    _capi.ERR_CHECKSUM: ChecksumError, _capi.ERR_MODEL_FORMAT: ModelFormatError}
+    if status in model_errors:
+        raise model_errors[status](msg)
     raise DeviceError(msg or f"spcv_cu status {status}")
 
 
@@ -289,9 +318,9 @@ class DeviceBcsr:
         return BcsrMatrix(self.rows, self.cols, self.block_h, rp, ci, va)
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and not getattr(self, "_borrowed", False):
             lib.spcv_cu_free(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -451,3 +480,72 @@ def spmm_layer(w: DeviceBcsr, act, bias, fused: Activation, out, residual=None,
         w.handle, act.data_ptr(), B, K, H, W, bptr, blen, fused.kind, fused.lo, fused.hi,
         None if residual is None else residual.data_ptr(), out.data_ptr(), out.shape[1],
         _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))
+
+
+# ------------------------------------------------------------ model files
+LAYER_KINDS = ("entry_conv", "pointwise", "depthwise", "global_pool", "fully_connected")
+
+
+def parse_model_status(data: bytes) -> int:
+    """spcv_cu_model_parse: 0 or the typed-error status (no device work)."""
+    buf = np.frombuffer(data, np.uint8)
+    n = ctypes.c_int()
+    return int(lib.spcv_cu_model_parse(buf.ctypes.data if buf.size else None, buf.size, ctypes.byref(n)))
+
+
+class DeviceModel:
+    """An SPCV model file (model_io.cpp) parsed with the reference's checks and
+    uploaded once: sparse 1x1 / classifier layers packed on the device."""
+
+    def __init__(self, data: bytes):
+        buf = np.frombuffer(data, np.uint8)
+        h = ctypes.c_void_p()
+        _raise(lib.spcv_cu_model_load(buf.ctypes.data if buf.size else None, buf.size, ctypes.byref(h)))
+        self._h = h
+        n = ctypes.c_int()
+        _raise(lib.spcv_cu_model_parse(buf.ctypes.data, buf.size, ctypes.byref(n)))
+        self.layers = []
+        info = np.zeros(12, np.int32)
+        for i in range(n.value):
+            _raise(lib.spcv_cu_model_layer(self._h, i, info.ctypes.data))
+            k = info.tolist()
+            self.layers.append(dict(kind=LAYER_KINDS[k[0]], cin=k[1], cout=k[2], in_h=k[3], in_w=k[4],
+                                    out_h=k[5], out_w=k[6], sparse=bool(k[7]), block_h=k[8],
+                                    act_kind=k[9], residual_src=k[10], stride=k[11]))
+
+    def weights(self, i: int) -> "DeviceBcsr":
+        """Borrowed packed weights of sparse layer i (valid while the model lives)."""
+        p = ctypes.c_void_p()
+        _raise(lib.spcv_cu_model_weights(self._h, i, ctypes.byref(p)))
+        L = self.layers[i]
+        w = DeviceBcsr.__new__(DeviceBcsr)
+        w._h, w._borrowed = p, True
+        w.cols, w.block_h = L["cin"], L["block_h"]
+        rows = ctypes.c_int()
+        nb = ctypes.c_size_t()
+        _raise(lib.spcv_cu_weights_info(p, ctypes.byref(rows), None, None, ctypes.byref(nb), None, None))
+        w.rows, w.nnz_blocks, w.row_slots, w.device = rows.value, nb.value, 0, 0
+        return w
+
+    def run(self, i: int, act, out, residual=None, strict: bool = True, stream=None) -> None:
+        """Layer i as run_network's pointwise step on torch CUDA tensors."""
+        import torch
+
+        B = act.shape[0]
+        if stream is None:
+            stream = torch.cuda.current_stream(act.device)
+        sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        _raise(lib.spcv_cu_model_run(self._h, i, act.data_ptr(), B,
+                                     None if residual is None else residual.data_ptr(), out.data_ptr(),
+                                     _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.spcv_cu_model_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,110 @@
+"""SPCV model files -> device.
+
+The parser (csrc/model.cu) restates parse_model (model_io.cpp:238-381): the
+same checks in the same order with the same typed errors. CPU tests pin it
+against the compiled reference on reference-written files and on thousands
+of mutated / truncated ones (the reference's own fuzz contract,
+test_model_io.cpp:166-188 and acceptance C10: only typed errors, never a
+crash). GPU tests load the file, compare every uploaded sparse layer with the
+reference's parsed arrays byte for byte, and run each 1x1 layer as
+run_network's pointwise step against the oracle.
+"""
+import numpy as np
+import pytest
+
+import paper_1911_09723_b200 as sp
+
+MODELS = [("mbv1", 0.25, 0.9), ("mbv2", 0.35, 0.8), ("ca-mbv2", 1.0, 0.85)]
+
+
+@pytest.fixture(scope="module")
+def files(ref):
+    return {f"{a}-{w}": ref.model_bytes(a, w, s, 7) for a, w, s in MODELS}
+
+
+def test_reference_files_parse(ref, files):
+    for name, data in files.items():
+        rc_ref, n_ref = ref.model_parse(data)
+        assert rc_ref == 0
+        assert sp.parse_model_status(data) == 0, name
+
+
+def test_canonical_errors_match_reference(ref, files):
+    data = files["mbv1-0.25"]
+    cases = {
+        "bad_magic": b"SPCX" + data[4:],
+        "version": data[:4] + bytes([2, 0]) + data[6:],
+        "empty": b"",
+        "short_magic": data[:3],
+        "truncated": data[:len(data) // 2],
+        "trailing": data + b"\x00",
+        "checksum": data[:-1] + bytes([data[-1] ^ 0xFF]),
+    }
+    want = {"bad_magic": 8, "version": 9, "empty": 10, "short_magic": 10, "truncated": 10,
+            "trailing": 12, "checksum": 11}
+    for k, blob in cases.items():
+        assert ref.model_parse(blob)[0] == want[k], k
+        assert sp.parse_model_status(blob) == want[k], k
+
+
+@pytest.mark.parametrize("name", [f"{a}-{w}" for a, w, _ in MODELS])
+def test_fuzz_typed_errors_match_reference(ref, files, name):
+    """Single-byte mutations (re-checksummed half the time so the structural
+    checks are reached) and truncations: our status == the reference's."""
+    import zlib
+
+    data = bytearray(files[name])
+    rng = np.random.default_rng(1234)
+    for trial in range(600):
+        blob = bytearray(data)
+        if trial % 5 == 4:
+            blob = blob[: int(rng.integers(0, len(blob)))]
+        else:
+            pos = int(rng.integers(0, len(blob) - 4))
+            blob[pos] = int(rng.integers(0, 256))
+            if trial % 2 == 0:  # fix the CRC so the mutation meets the semantic checks
+                blob[-4:] = zlib.crc32(bytes(blob[:-4])).to_bytes(4, "little")
+        blob = bytes(blob)
+        assert sp.parse_model_status(blob) == ref.model_parse(blob)[0], (trial, len(blob))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [f"{a}-{w}" for a, w, _ in MODELS])
+def test_device_model_matches_reference_layers(ref, oracle, files, name):
+    import torch
+
+    data = files[name]
+    m = sp.DeviceModel(data)
+    rng = np.random.default_rng(3)
+    checked = 0
+    for i, L in enumerate(m.layers):
+        if L["kind"] not in ("pointwise", "fully_connected"):
+            continue
+        meta, (rp, ci, va, bias) = ref.model_layer(data, i)
+        assert (meta["cin"], meta["cout"]) == (L["cin"], L["cout"])
+        if not L["sparse"]:
+            continue
+        w = m.weights(i)
+        back = w.unpack()
+        assert back.row_ptr.tobytes() == rp.tobytes()
+        assert back.col_idx.tobytes() == ci.tobytes()
+        assert back.values.tobytes() == va.tobytes()
+        # run_network's pointwise step: padded rows, zero pad bias, truncation, residual
+        B, H, W = 2, L["in_h"], L["in_w"]
+        act = rng.uniform(-1, 1, (B, L["cin"], H, W)).astype(np.float32)
+        mat = sp.BcsrMatrix(meta["rows"], meta["cols"], meta["block_h"], rp, ci, va)
+        pad = meta["rows"] - L["cout"]
+        fused = ("none", 0, 0) if L["act_kind"] == 0 else ("clamp", 0.0, 6.0)
+        want = oracle.spmm(mat, act, np.r_[bias, np.zeros(pad, np.float32)], fused)[:, :L["cout"]]
+        want = want.reshape(B, L["cout"], L["out_h"], L["out_w"])
+        res = None
+        if L["residual_src"] >= 0:
+            res = rng.uniform(-1, 1, want.shape).astype(np.float32)
+            want = (want + res).astype(np.float32)
+        out = torch.empty(want.shape, device="cuda")
+        m.run(i, torch.from_numpy(act).cuda(), out,
+              None if res is None else torch.from_numpy(res).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), L
+        checked += 1
+    assert checked > 5
