@@ -87,6 +87,17 @@ int spcv_cu_weights_info(const spcv_cu_weights* w, int* rows, int* cols, int* bl
 
 void spcv_cu_free(spcv_cu_weights* w);
 
+/* Which CUDA kernel spmm runs for these weights in `mode`:
+ *   SPCV_KERNEL_TILE — the shared-memory tile kernel (any K up to the tile limit);
+ *   SPCV_KERNEL_JIT  — a kernel specialised on this matrix's structure and
+ *                      values (K <= 128 and <= 16384 stored weights), compiled
+ *                      with NVRTC on first use and cached in the weights.
+ * Compiles the specialised kernel if it is due and not built yet. Both kernels
+ * are bit-exact in SPCV_MODE_STRICT. SPCV_JIT=0 in the environment at pack
+ * time selects the tile kernel. No reference counterpart (introspection). */
+enum { SPCV_KERNEL_TILE = 0, SPCV_KERNEL_JIT = 1 };
+int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel);
+
 /* spmm_into over a batch of `images` CHW images on device memory:
  *   act [images][act_c][act_h*act_w], out [images][out_c][out_h*out_w].
  *   out[i][c][s] = fused(bias[c] + sum over c's stored blocks of value*act[i][col][s])

@@ -18,6 +18,7 @@ ERR_MODEL_IO, ERR_BAD_MAGIC, ERR_VERSION, ERR_TRUNCATED, ERR_CHECKSUM, ERR_MODEL
 LAYOUT_CHW, LAYOUT_HWC = 0, 1
 ACT_NONE, ACT_CLAMP = 0, 1
 MODE_STRICT, MODE_FAST = 0, 1
+KERNEL_TILE, KERNEL_JIT = 0, 1
 
 # Every symbol include/spcv_cu.h declares, with (restype, argtypes).
 _p, _i, _f, _z, _u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t, ctypes.c_uint64
@@ -27,6 +28,7 @@ SIGNATURES = {
     "spcv_cu_unpack": (_i, [_p, _p, _p, _p]),
     "spcv_cu_weights_info": (_i, [_p, _p, _p, _p, _p, _p, _p]),
     "spcv_cu_free": (None, [_p]),
+    "spcv_cu_weights_kernel": (_i, [_p, _i, _p]),
     "spcv_cu_spmm_into": (_i, _SPMM_ARGS + [_p]),
     "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
     "spcv_cu_spmm_layer": (_i, [_p, _p, _i, _i, _i, _i, _p, _z, _i, _f, _f, _p, _p, _i, _i, _p]),

@@ -139,6 +139,7 @@ void free_weights(spcv_cu_weights* w) {
     cudaFree(w->d_values);
     cudaFree(w->d_stream);
     cudaFree(w->d_bin_beg);
+    jit_release(w);
     delete w;
 }
 
@@ -316,6 +317,18 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     w->nblocks = nblocks;
     w->nchunks = cur;
     cudaGetDevice(&w->device);
+    // Small-K matrices also get a weight-specialised kernel (jit.cu), compiled
+    // on first use. SPCV_JIT=0 disables it, so the tile kernel runs everywhere.
+    {
+        const char* e = std::getenv("SPCV_JIT");
+        const bool off = e && std::atoi(e) == 0;
+        w->jit_eligible = !off && cols <= kJitMaxK && nvalues <= kJitMaxWeights;
+        if (w->jit_eligible) {
+            w->h_row_ptr.assign(row_ptr, row_ptr + brows + 1);
+            w->h_col_idx.assign(col_idx, col_idx + nblocks);
+            w->h_values.assign(values, values + nvalues);
+        }
+    }
     int rc = SPCV_OK;
     if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
         (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
@@ -373,6 +386,29 @@ extern "C" int spcv_cu_weights_info(const spcv_cu_weights* w, int* rows, int* co
 }
 
 extern "C" void spcv_cu_free(spcv_cu_weights* w) { free_weights(w); }
+
+extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel) {
+    g_last_error.clear();
+    // probe with the plain spmm_into shape (bias, clamp, all rows)
+    if (!w || !kernel) return fail(SPCV_ERR_INVALID, "spcv_cu_weights_kernel: null argument");
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "spcv_cu_weights_kernel: unknown arithmetic mode");
+    *kernel = SPCV_KERNEL_TILE;
+    if (w->jit_eligible) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        SPCV_CUDA(cudaSetDevice(w->device));
+        JitKey key;
+        key.strict = mode == SPCV_MODE_STRICT;
+        key.clamp = true;
+        key.bias = true;
+        key.vec = true;
+        key.m_out = w->rows;
+        if (jit_prepare(w, key)) *kernel = SPCV_KERNEL_JIT;
+        cudaSetDevice(prev);
+    }
+    return SPCV_OK;
+}
 
 // ------------------------------------------------------------------- launch
 
@@ -445,6 +481,19 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(residual) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
+    if (w->jit_eligible) {
+        // const_cast: the compiled kernel is a cache inside the weights object
+        // A failed compile (recorded, never retried) falls back to the tile kernel.
+        JitKey key;
+        key.strict = strict;
+        key.clamp = act_kind == SPCV_ACT_CLAMP;
+        key.bias = bias != nullptr;
+        key.res = residual != nullptr;
+        key.vec = S % 4 == 0 && reinterpret_cast<uintptr_t>(act) % 16 == 0;
+        key.m_out = a.M_out;
+        if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key))
+            return jit_launch(v, w->cols, sms, a, st);
+    }
     switch (w->block_h) {
         case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);
         case 2: return launch_bh2(a, w, ntiles, sms, strict, vec, st);

@@ -8,9 +8,28 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "../../include/spcv_cu.h"
 #include "spmm_kernel.cuh"
+
+// A weight-specialised kernel compiled at run time (jit.cu), one per call
+// shape: arithmetic mode, activation kind, bias/residual presence, stored rows.
+struct JitKey {
+    bool strict = true, clamp = false, bias = false, res = false;
+    bool vec = false;  // S % 4 == 0 and 16 B aligned activations: 16 B copies
+    int m_out = 0;
+    bool operator==(const JitKey& o) const {
+        return strict == o.strict && clamp == o.clamp && bias == o.bias && res == o.res &&
+               vec == o.vec && m_out == o.m_out;
+    }
+};
+struct JitVariant {
+    JitKey key;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fn = nullptr;  // null: not built (over budget, or compile/load failed)
+    int blocks_per_sm = 0;
+};
 
 struct spcv_cu_weights {
     int rows = 0, cols = 0, block_h = 1, brows = 0;
@@ -29,6 +48,11 @@ struct spcv_cu_weights {
     // execution schedule
     uint4* d_stream = nullptr;
     uint32_t* d_bin_beg = nullptr;
+    // small-K path (jit.cu): host copy of the matrix and the compiled variants
+    bool jit_eligible = false;
+    std::vector<uint32_t> h_row_ptr, h_col_idx;
+    std::vector<float> h_values;
+    std::vector<JitVariant> jit;
 };
 
 namespace spcv_detail {
@@ -54,6 +78,25 @@ int launch_bh2(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
                bool strict, bool vec, cudaStream_t);
 int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntiles, int sms,
                bool strict, bool vec, cudaStream_t);
+
+// Weight-specialised kernels for small K (jit.cu).
+constexpr int kJitMaxK = 128;             // activation registers per thread
+constexpr size_t kJitMaxWeights = 16384;  // host copy kept for matrices up to this size
+constexpr int kJitMaxInstr = 4608;        // straight-line code budget (instruction cache)
+// One CTA per SM: W warps, P prefetch stages of a [K][32] fp32 slot per warp.
+struct JitGeometry {
+    int warps, stages, smem;
+};
+inline JitGeometry jit_geometry(int K) {
+    const int slot = K * 32 * 4;
+    int warps = K <= 64 ? 16 : 12;
+    int stages = 1;
+    while (stages < 3 && warps * slot * (stages + 1) <= 200 * 1024) ++stages;
+    return {warps, stages, warps * slot * stages};
+}
+const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
+int jit_launch(const JitVariant* v, int K, int sms, const spcvk::KernelArgs& a, cudaStream_t st);
+void jit_release(spcv_cu_weights* w);
 
 }  // namespace spcv_detail
 

@@ -309,6 +309,14 @@ class DeviceBcsr:
     def handle(self):
         return self._h
 
+    def kernel(self, strict: bool = True) -> str:
+        """Which CUDA kernel runs these weights: "tile" or "jit" (spcv_cu_weights_kernel;
+        compiles the weight-specialised kernel if it is due)."""
+        k = ctypes.c_int()
+        _raise(lib.spcv_cu_weights_kernel(self._h, _capi.MODE_STRICT if strict else _capi.MODE_FAST,
+                                          ctypes.byref(k)))
+        return "jit" if k.value == _capi.KERNEL_JIT else "tile"
+
     def unpack(self) -> BcsrMatrix:
         """Bit-exact device decode of the counts/deltas/values streams."""
         rp = np.zeros(self.rows // self.block_h + 1, dtype=np.uint32)

@@ -483,6 +483,7 @@ def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, cas
     and lane width the packer would otherwise pick. Every combination must
     equal the oracle bit-for-bit."""
     monkeypatch.setenv("SPCV_PIPELINE", pipeline)
+    monkeypatch.setenv("SPCV_JIT", "0")  # small K would otherwise take the JIT kernel
     env = {"steps2": {"SPCV_STEPS": "2"}, "steps4": {"SPCV_STEPS": "4"}, "nf2": {"SPCV_NF": "2"},
            "nf4_steps2": {"SPCV_NF": "4", "SPCV_STEPS": "2"}}.get(layout, {})
     for k, v in env.items():
@@ -494,6 +495,50 @@ def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, cas
     assert np.array_equal(bits(got), bits(want))
     fast = run_device(d.weights, d.act, d.bias, layer.act, strict=False)
     check_tolerance(d, fast, want)
+
+
+# ------------------------------------ weight-specialised small-K kernel (jit.cu)
+JIT_CASES = [
+    ("pw1", mbv1_pointwise()[0], 2),
+    ("pw2", mbv1_pointwise()[1], 1),
+    ("pw3", mbv1_pointwise()[2], 1),
+    ("bh2_odd", Layer("b2", 96, 64, 7, 9, ("clamp", 0.0, 6.0), -1.0, 1.0, 0.8, 2), 5),
+    ("bh4_none", Layer("b4", 128, 128, 5, 5, ("none", 0.0, 0.0), -1.0, 1.0, 0.9, 4), 4),
+    ("k1", Layer("k1", 1, 8, 3, 3, ("none", 0.0, 0.0), -1.0, 1.0, 0.0), 2),
+    ("dense", Layer("d", 16, 32, 4, 4, sparsity=0.0), 2),
+    ("empty_rows", Layer("e", 32, 40, 3, 5, ("clamp", -0.5, 0.5), -1.0, 1.0, 0.97), 3),
+]
+
+
+@pytest.mark.parametrize("kernel", ["jit", "tile"])
+@pytest.mark.parametrize("case", JIT_CASES, ids=lambda c: c[0])
+def test_jit_and_tile_small_k_bit_exact(oracle, monkeypatch, kernel, case):
+    """K <= 128: the weight-specialised kernel (SPCV_JIT default) and the tile
+    kernel (SPCV_JIT=0) both equal the oracle bit-for-bit in strict mode, with
+    and without bias, and stay within the fast-mode bound."""
+    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    _, layer, images = case
+    d = make_layer_data(layer, images, 99)
+    dw = sp.DeviceBcsr(d.weights)
+    assert dw.kernel(strict=True) == kernel and dw.kernel(strict=False) == kernel
+    got = run_device(d.weights, d.act, d.bias, layer.act, dw=dw)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
+    got0 = run_device(d.weights, d.act, None, layer.act, dw=dw)
+    want0 = oracle.spmm(d.weights, d.act, None, layer.act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got0), bits(want0))
+    check_tolerance(d, run_device(d.weights, d.act, d.bias, layer.act, strict=False, dw=dw), want)
+
+
+def test_jit_not_used_beyond_its_limits(monkeypatch):
+    monkeypatch.delenv("SPCV_JIT", raising=False)
+    big_k = make_layer_data(Layer("k", 129, 8, 2, 2, sparsity=0.5), 1, 1)
+    assert sp.DeviceBcsr(big_k.weights).kernel() == "tile"
+    small = make_layer_data(Layer("s", 128, 8, 2, 2, sparsity=0.5), 1, 1)
+    assert sp.DeviceBcsr(small.weights).kernel() == "jit"
+    # MBv1 pw4 (3.3k weights): over the straight-line code budget in both modes
+    pw4 = sp.DeviceBcsr(make_layer_data(mbv1_pointwise()[3], 1, 1).weights)
+    assert pw4.kernel(strict=True) == "tile" and pw4.kernel(strict=False) == "tile"
 
 
 # ------------------------------------------------- dense fp32 baseline (§8f-1)
@@ -540,9 +585,10 @@ def test_dense_baseline_validation_order():
 
 
 # ------------------------------- executor pointwise step on device (§8f-2)
+@pytest.mark.parametrize("kernel", ["jit", "tile"])
 @pytest.mark.parametrize("hw", [(7, 9), (8, 8)], ids=["odd_spatial", "vec"])
 @pytest.mark.parametrize("bh", [2, 4])
-def test_spmm_layer_padded_rows_and_residual(oracle, hw, bh):
+def test_spmm_layer_padded_rows_and_residual(oracle, monkeypatch, hw, bh, kernel):
     """run_network's pointwise branch (netdef.cpp:494-512): weights padded to
     the block height are run wide (pad rows bias 0) and truncated to the
     logical rows; the residual is added after the activation. Bit-exact
@@ -562,7 +608,9 @@ def test_spmm_layer_padded_rows_and_residual(oracle, hw, bh):
     res = rng.uniform(-1, 1, (B, rows, H, W)).astype(np.float32)
     want = oracle.spmm(m, act, np.r_[bias, np.zeros(pad, np.float32)], RELU6)[:, :rows].reshape(B, rows, H, W)
     want_res = (want + res).astype(np.float32)
+    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
     dw = sp.DeviceBcsr(m)
+    assert dw.kernel() == kernel
     a = torch.from_numpy(act).cuda()
     o = torch.full((B, rows, H, W), float("nan"), device="cuda")
     sp.spmm_layer(dw, a, torch.from_numpy(bias).cuda(), RELU6, o)

@@ -47,6 +47,51 @@ def test_cabi_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
+def _jit_compile(m, mode, act_kind=1, has_bias=1, has_res=0, m_out=None):
+    lib = ctypes.CDLL(os.path.join(LIBDIR, "libspcv_cu.so"))
+    fn = lib.spcvx_jit_compile
+    P, Z, I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    fn.argtypes = [I, I, I, P, P, Z, P, I, I, I, I, I, ctypes.POINTER(Z), ctypes.POINTER(Z),
+                   ctypes.c_char_p, Z]
+    rp = np.ascontiguousarray(m.row_ptr, np.uint32)
+    ci = np.ascontiguousarray(m.col_idx, np.uint32)
+    va = np.ascontiguousarray(m.values, np.float32)
+    sb, cb = Z(), Z()
+    buf = ctypes.create_string_buffer(1 << 20)
+    rc = fn(m.rows, m.cols, m.block_h, rp.ctypes.data, ci.ctypes.data if ci.size else None, ci.size,
+            va.ctypes.data if va.size else None, mode, act_kind, has_bias, has_res,
+            m.rows if m_out is None else m_out, ctypes.byref(sb), ctypes.byref(cb), buf, 1 << 20)
+    return rc, buf.value.decode(), cb.value
+
+
+def test_jit_kernel_source_and_nvrtc_compile_without_gpu():
+    """The small-K kernel (jit.cu) is generated from the matrix and compiled by
+    NVRTC for sm_100a; neither step needs a device. Every stored weight appears
+    once per row as an exact hex-float immediate, in ascending column order."""
+    rng = np.random.default_rng(3)
+    dense = rng.standard_normal((12, 20)).astype(np.float32)
+    dense[rng.random((12, 20)) < 0.7] = 0
+    m = sp.encode_bcsr(dense, 2)
+    rc, src, cubin = _jit_compile(m, _capi.MODE_STRICT)
+    assert rc == 0 and cubin > 0
+    assert src.count("__fmul_rn(") == m.nnz_values() and "__fmaf_rn" not in src
+    rp, ci, va = np.asarray(m.row_ptr), np.asarray(m.col_idx), np.asarray(m.values)
+    for r in range(12):  # stored blocks of r's block row, zeros inside blocks included
+        blks = range(rp[r // 2], rp[r // 2 + 1])
+        body = src.split("__stcs(o + %dLL * S" % r)[0].rsplit("{", 1)[1]
+        imms = re.findall(r"__fmul_rn\(\(?([^,()]*)\)?, x(\d+)\)", body)
+        assert [int(k) for _, k in imms] == [int(ci[b]) for b in blks]
+        got = np.array([float.fromhex(v.rstrip("f")) if "0x" in v else float(v.rstrip("f"))
+                        for v, _ in imms], np.float32)
+        want = np.array([va[2 * b + r % 2] for b in blks], np.float32)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    rc, src, _ = _jit_compile(m, _capi.MODE_FAST, act_kind=0, has_bias=0, has_res=1, m_out=11)
+    assert rc == 0
+    assert src.count("__fmaf_rn(") == sum(2 * (rp[i + 1] - rp[i]) for i in range(5)) + rp[6] - rp[5]
+    assert "lo ?" not in src
+    assert "__stcs(o + 11LL" not in src and "__ldcs(r + 10LL" in src
+
+
 def test_cpp_dropin_library_exports_reference_api():
     so = os.path.join(LIBDIR, "libspcv_b200.so")
     out = subprocess.run(["nm", "-DC", so], capture_output=True, text=True).stdout

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Run one workload layer's SpMM kernel a few times (for ncu / quick timing).
 
-  python tools/prof_layer.py --config c2-b256 --layer pw7 [--reps 5] [--mode fast]
+  python tools/prof_layer.py --config c2-b256 --layer pw7[,pw8...] [--reps 5] [--mode fast]
 
 Prints per-launch CUDA-event times; under ncu use -k regex:spmm_bcsr -s <warmups>.
 """
@@ -30,7 +30,11 @@ def main():
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     layers = {L.name: (i, L) for i, L in enumerate(cfg["layers"]())}
-    li, L = layers[args.layer]
+    for name in args.layer.split(","):
+        run_layer(args, cfg, *layers[name], name)
+
+
+def run_layer(args, cfg, li, L, name):
     images = args.images or cfg["images"]
     d = make_layer_data(L, images, 1000 * (li + 1))
     dw = sp.DeviceBcsr(d.weights)
@@ -51,7 +55,7 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     us = statistics.median(ts)
-    print(f"{args.layer} K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
+    print(f"{name} kernel={dw.kernel(args.mode == 'strict')} K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
           f"median {us:.1f} us  {d.flops() / us / 1e3:.0f} GFLOP/s  {d.alg_bytes() / us / 1e3:.0f} GB/s "
           f"(alg bytes {d.alg_bytes():.0f})")
 
