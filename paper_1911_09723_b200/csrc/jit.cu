@@ -1,17 +1,33 @@
-// jit.cu — weight-specialised SpMM kernels for small input-channel counts.
+// jit.cu — weight-specialised SpMM kernels (NVRTC, compiled on first use).
 //
-// For K <= 128 the whole activation column of an image fits in registers, so
-// the sparse structure and the weights themselves can be compiled into the
-// instruction stream (NVRTC at pack time): each thread loads its columns'
-// K activations once (coalesced across the warp, straight from HBM), then
-// every stored weight becomes one FMUL-with-immediate + FADD (strict) or one
-// FFMA-with-immediate (fast). There is no shared-memory gather and no weight
-// stream: the per-FMA cost is instruction issue, which for these layers is
-// far below the HBM time, so the layer runs at the HBM roof.
+// The tile kernel (spmm_kernel.cuh) is bound by its shared-memory gather: one
+// activation load per stored weight per column. Here the sparse structure and
+// the weights are compiled into the instruction stream instead:
 //
-// Arithmetic is the reference's per-element order exactly (bias first, blocks
-// in ascending column, __fmul_rn then __fadd_rn, ternary clamp:
-// kernels.cpp:14-43), so strict mode stays bit-exact.
+//  * k-major order. A warp owns a group of 64 virtual columns (2 per lane,
+//    f32x2 registers) and keeps one accumulator pair per output row of its
+//    row segment in registers. Activation rows stream through shared memory
+//    in chunks of 32 channels (cp.async, P-deep ring per warp); each channel
+//    pair is loaded once (LDS.64) and feeds every row of the segment that
+//    stores a block at that channel, as FMUL2-with-immediate + FFMA2 (strict)
+//    or FFMA2-with-immediate (fast). Per row the terms still arrive in
+//    ascending channel order after the bias (kernels.cpp:14-43), so strict
+//    mode is bit-exact: fma.rn.f32x2(acc, 1.0, p) rounds acc + p once, exactly
+//    like add.rn (the 1.0 is a kernel argument so ptxas cannot fold the pair
+//    back into a fused multiply-add).
+//
+//  * Row segments across SMs. Straight-line code only runs at full rate while
+//    it fits the SM's instruction cache, so the rows are cut into segments of
+//    at most ~kJitSegInstr instructions and one persistent CTA per SM runs one
+//    segment; SMs are shared out in proportion to segment cost. The segments
+//    sweep the column groups in the same order at the same rate, so the
+//    activations each group needs are read from HBM once and served to the
+//    other segments from L2.
+//
+// Clamp is the ternary compare of Activation::apply (tensor.hpp:90-96), done
+// per column on the unpacked pair. Rows >= m_out (padding of a model layer,
+// netdef.cpp:496-505) are not generated. Requires S % 4 == 0 and 16 B aligned
+// activations (key.vec); other shapes use the tile kernel.
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -30,159 +46,229 @@ using namespace spcv_detail;
 
 namespace {
 
-std::string hexf(float v) {
-    // exact C99 hex float literal (no decimal rounding)
-    char buf[48];
-    if (v == 0.0f) return std::signbit(v) ? "(-0.0f)" : "0.0f";
-    std::snprintf(buf, sizeof buf, "%af", static_cast<double>(v));
-    return std::string("(") + buf + ")";
+constexpr int kKC = 32;        // channels per staged chunk
+constexpr int kCols = 64;      // columns per warp group (2 per lane)
+constexpr int kRowsMax = 64;   // rows per segment (2 accumulator registers each)
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
 }
 
-// CUDA C for one matrix and one call shape (JitKey).
-//
-// One persistent CTA per SM of W warps (jit_geometry). Rounds: in each round
-// warp w of CTA c owns the group of 32 virtual columns (image, pixel)
-// g = round * gridDim.x * W + c * W + w, one column per lane. A group's K
-// activation rows are copied global -> shared with cp.async into a per-warp
-// [k][32] slot (16 B copies of 4 columns when key.vec), P rounds ahead, so
-// HBM reads overlap the math of earlier rounds. A CTA barrier per round
-// keeps the W warps in step: they execute the same straight-line code at the
-// same time, which keeps the instruction-cache working set small.
-//
-// Math: each lane moves its column into registers (conflict-free LDS), then
-// every stored weight is an immediate operand of FMUL+FADD (strict) or FFMA
-// (fast); rows are emitted 4 at a time interleaved term by term (each row's
-// own order unchanged: bias first, blocks ascending, kernels.cpp:14-43) to
-// hide the add latency. Bias presence, activation kind, residual and the
-// stored row count are compile-time; rows >= m_out (padding of a model layer,
-// netdef.cpp:496-505) are not generated. Clamp is the ternary compare of
-// Activation::apply (tensor.hpp:90-96).
-std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
-                       size_t nblocks, const float* values, const JitKey& key) {
-    const JitGeometry geo = jit_geometry(K);
-    const int W = geo.warps, P = geo.stages;
-    std::ostringstream o;
-    o << "#define K " << K << "LL\n#define W " << W << "\n#define P " << P << "\n"
-      << "__device__ __forceinline__ unsigned sa(const void* p) {"
-         " return (unsigned)__cvta_generic_to_shared(p); }\n"
-      << "__device__ __forceinline__ void cp16(float* d, const float* s) {"
-         " asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sa(d)), \"l\"(s) : \"memory\"); }\n"
-      << "__device__ __forceinline__ void cp4(float* d, const float* s) {"
-         " asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: \"r\"(sa(d)), \"l\"(s) : \"memory\"); }\n"
-      << "extern \"C\" __global__ void __launch_bounds__(W * 32, 1)"
-         " spcv_jit(const float* __restrict__ act, float* __restrict__ out,"
-         " const float* __restrict__ bias, long long N, long long S, float lo, float hi,"
-         " const float* __restrict__ res) {\n"
-      << "  extern __shared__ float4 smem4[];\n"
-      << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-      << "  float* slot0 = reinterpret_cast<float*>(smem4) + warp * (K * 32);\n"
-      << "  const long long G = (N + 31) >> 5, per_round = (long long)gridDim.x * W;\n"
-      << "  const long long first = (long long)blockIdx.x * W + warp;\n"
-      << "  const long long rounds = (G - (long long)blockIdx.x * W + per_round - 1) / per_round;\n"
-      << "  auto issue = [&](long long r) {\n"
-      << "    const long long gg = first + r * per_round;\n"
-      << "    float* xs = slot0 + (r % P) * (W * K * 32);\n";
-    if (key.vec)
-        o << "    const long long nq = gg * 32 + 4 * (lane & 7);\n"
-          << "    if (r < rounds && nq < N) {\n"
-          << "      const long long b = nq / S, s = nq - b * S;\n"
-          << "      const float* src = act + b * K * S + s;\n"
-          << "      float* dst = xs + 4 * (lane & 7);\n"
-          << "#pragma unroll 8\n"
-          << "      for (int k = lane >> 3; k < K; k += 4) cp16(dst + k * 32, src + k * S);\n"
-          << "    }\n";
-    else
-        o << "    const long long n = gg * 32 + lane;\n"
-          << "    if (r < rounds && n < N) {\n"
-          << "      const long long b = n / S, s = n - b * S;\n"
-          << "      const float* src = act + b * K * S + s;\n"
-          << "#pragma unroll 8\n"
-          << "      for (int k = 0; k < K; ++k) cp4(xs + k * 32 + lane, src + k * S);\n"
-          << "    }\n";
-    o << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n"
-      << "  };\n"
-      << "#pragma unroll 1\n"
-      << "  for (int r = 0; r < P; ++r) issue(r);\n"
-      << "#pragma unroll 1\n"
-      << "  for (long long r = 0; r < rounds; ++r) {\n"
-      << "    asm volatile(\"cp.async.wait_group %0;\" :: \"n\"(P - 1) : \"memory\");\n"
-      << "    __syncthreads();\n"
-      << "    const float* xs = slot0 + (r % P) * (W * K * 32);\n";
-    std::vector<char> used(static_cast<size_t>(K), 0);
-    for (size_t b = 0; b < nblocks; ++b) used[col_idx[b]] = 1;
-    for (int k = 0; k < K; ++k)
-        if (used[k]) o << "    const float x" << k << " = xs[" << k * 32 << " + lane];\n";
-    o << "    __syncwarp();\n"
-      << "    issue(r + P);\n"
-      << "    const long long n = (first + r * per_round) * 32 + lane;\n"
-      << "    if (n >= N) continue;\n"
-      << "    const long long b = n / S, s = n - b * S;\n"
-      << "    float* o = out + b * " << key.m_out << "LL * S + s;\n";
-    if (key.res) o << "    const float* rp = res + b * " << key.m_out << "LL * S + s;\n";
-    // stored rows, emitted kIL at a time with their terms interleaved
-    constexpr int kIL = 4;
-    std::vector<int> rows;
-    for (int r = 0; r < std::min(M, key.m_out); ++r) rows.push_back(r);
-    for (size_t r0 = 0; r0 < rows.size(); r0 += kIL) {
-        const size_t r1 = std::min(rows.size(), r0 + kIL);
-        o << "    {\n";
-        size_t longest = 0;
-        for (size_t q = r0; q < r1; ++q) {
-            const int row = rows[q], br = row / BH;
-            longest = std::max<size_t>(longest, row_ptr[br + 1] - row_ptr[br]);
-            o << "      float a" << q - r0 << " = "
-              << (key.bias ? "__ldg(bias + " + std::to_string(row) + ")" : "0.0f") << ";\n";
+// f32 bit pattern duplicated into both halves of a .b64 (f32x2 broadcast).
+std::string imm2(float v) {
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "0x%08x%08xULL", u, u);
+    return buf;
+}
+
+struct Segment {
+    int r0 = 0, r1 = 0;      // stored rows [r0, r1)
+    long long instr = 0;     // straight-line instructions per column group
+    int ctas = 0;
+};
+
+int row_nnz(const uint32_t* row_ptr, int BH, int r) {
+    return static_cast<int>(row_ptr[r / BH + 1] - row_ptr[r / BH]);
+}
+
+// Cut rows [0, m_out) into segments (contiguous rows, cost <= budget, at most
+// kRowsMax rows) and share `sms` CTAs out in proportion to their cost.
+bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key,
+                   std::vector<Segment>& segs) {
+    const int budget = env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr);
+    const int max_segs = std::min(env_int("SPCV_JIT_MAX_SEGS", kJitMaxSegs), key.sms);
+    const int per_weight = key.strict ? 2 : 1;
+    const int nkc = (K + kKC - 1) / kKC;
+    const long long fixed = static_cast<long long>(nkc) * 24 + K;  // copies, waits, LDS.64
+    const int rows = std::min(M, key.m_out);
+    segs.clear();
+    Segment cur;
+    cur.instr = fixed;
+    for (int r = 0; r < rows; ++r) {
+        const long long c = static_cast<long long>(per_weight) * row_nnz(row_ptr, BH, r) + 10;
+        if (cur.r1 > cur.r0 && (cur.instr + c > budget || cur.r1 - cur.r0 == kRowsMax)) {
+            segs.push_back(cur);
+            cur = Segment();
+            cur.r0 = cur.r1 = r;
+            cur.instr = fixed;
         }
-        for (size_t t = 0; t < longest; ++t) {
-            for (size_t q = r0; q < r1; ++q) {
-                const int row = rows[q], br = row / BH, i = row % BH;
-                if (t >= row_ptr[br + 1] - row_ptr[br]) continue;
-                const uint32_t blk = row_ptr[br] + static_cast<uint32_t>(t);
-                const std::string A = "a" + std::to_string(q - r0);
-                const std::string wv = hexf(values[static_cast<size_t>(blk) * BH + i]);
-                const std::string x = "x" + std::to_string(col_idx[blk]);
-                if (key.strict)
-                    o << "      " << A << " = __fadd_rn(" << A << ", __fmul_rn(" << wv << ", " << x << "));\n";
-                else
-                    o << "      " << A << " = __fmaf_rn(" << wv << ", " << x << ", " << A << ");\n";
+        cur.r1 = r + 1;
+        cur.instr += c;
+    }
+    if (cur.r1 > cur.r0) segs.push_back(cur);
+    if (segs.empty() || static_cast<int>(segs.size()) > max_segs) return false;
+    long long total = 0;
+    for (const Segment& s : segs) total += s.instr;
+    int given = 0;
+    for (Segment& s : segs) {
+        s.ctas = std::max(1, static_cast<int>(static_cast<double>(key.sms) * s.instr / total));
+        given += s.ctas;
+    }
+    // hand out the remainder / take back the excess by cost per CTA
+    while (given != key.sms) {
+        int best = -1;
+        double bv = 0;
+        for (size_t i = 0; i < segs.size(); ++i) {
+            const double load = static_cast<double>(segs[i].instr) / segs[i].ctas;
+            if (given < key.sms) {
+                if (best < 0 || load > bv) best = static_cast<int>(i), bv = load;
+            } else if (segs[i].ctas > 1) {
+                const double after = static_cast<double>(segs[i].instr) / (segs[i].ctas - 1);
+                if (best < 0 || after < bv) best = static_cast<int>(i), bv = after;
             }
         }
-        for (size_t q = r0; q < r1; ++q) {
-            const int row = rows[q];
-            const std::string A = "a" + std::to_string(q - r0);
-            if (key.clamp) o << "      " << A << " = " << A << " < lo ? lo : (" << A << " > hi ? hi : " << A << ");\n";
-            if (key.res) o << "      " << A << " = __fadd_rn(" << A << ", __ldcs(rp + " << row << "LL * S));\n";
-            o << "      __stcs(o + " << row << "LL * S, " << A << ");\n";
-        }
-        o << "    }\n";
+        if (best < 0) return false;
+        segs[best].ctas += given < key.sms ? 1 : -1;
+        given += given < key.sms ? 1 : -1;
     }
+    return true;
+}
+
+std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
+                       const float* values, const JitKey& key, const std::vector<Segment>& segs) {
+    const int nkc = (K + kKC - 1) / kKC;
+    std::ostringstream o;
+    o << "#define K " << K << "LL\n#define KC " << kKC << "\n#define NKC " << nkc
+      << "\n#define W " << kJitWarps << "\n#define P " << kJitStages << "\n"
+      << "typedef unsigned long long u64;\n"
+      << "__device__ __forceinline__ unsigned sa(const void* p) {"
+         " return (unsigned)__cvta_generic_to_shared(p); }\n"
+      << "#define CP16(d, off, s) asm volatile(\"cp.async.cg.shared.global [%0+\" #off \"], [%1], 16;\" :: \"r\"(d), \"l\"(s) : \"memory\")\n"
+      << "#define LDS64(v, a, off) asm volatile(\"ld.shared.b64 %0, [%1+\" #off \"];\" : \"=l\"(v) : \"r\"(a))\n"
+      << "__device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 d;"
+         " asm(\"mul.rn.f32x2 %0, %1, %2;\" : \"=l\"(d) : \"l\"(a), \"l\"(b)); return d; }\n"
+      << "__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 d;"
+         " asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(d) : \"l\"(a), \"l\"(b), \"l\"(c)); return d; }\n"
+      << "__device__ __forceinline__ u64 dup(float f) {"
+         " return ((u64)__float_as_uint(f) << 32) | __float_as_uint(f); }\n"
+      << "__device__ __forceinline__ float lo32(u64 v) { return __uint_as_float((unsigned)v); }\n"
+      << "__device__ __forceinline__ float hi32(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }\n"
+      << "__device__ __forceinline__ float clampf(float v, float lo, float hi) {"
+         " return v < lo ? lo : (v > hi ? hi : v); }\n";
+    // CTA -> (segment, rank in segment)
+    o << "__device__ const unsigned char seg_of[" << key.sms << "] = {";
+    for (size_t s = 0; s < segs.size(); ++s)
+        for (int c = 0; c < segs[s].ctas; ++c) o << s << ",";
+    o << "};\n__device__ const unsigned char rank_of[" << key.sms << "] = {";
+    for (size_t s = 0; s < segs.size(); ++s)
+        for (int c = 0; c < segs[s].ctas; ++c) o << c << ",";
+    o << "};\n";
+
+    const int brows = M / BH;
+    std::vector<std::vector<std::pair<int, float>>> by_k;  // (row in segment, weight) per channel
+    for (size_t si = 0; si < segs.size(); ++si) {
+        const Segment& sg = segs[si];
+        const int R = sg.r1 - sg.r0;
+        by_k.assign(static_cast<size_t>(K), {});
+        for (int r = sg.r0; r < sg.r1; ++r) {
+            const int br = r / BH, i = r % BH;
+            if (br >= brows) continue;
+            for (uint32_t b = row_ptr[br]; b < row_ptr[br + 1]; ++b)
+                by_k[col_idx[b]].emplace_back(r - sg.r0, values[static_cast<size_t>(b) * BH + i]);
+        }
+        o << "__device__ __forceinline__ void seg" << si
+          << "(const float* __restrict__ act, float* __restrict__ out, const float* __restrict__ bias,"
+             " long long N, long long S, float lo, float hi, const float* __restrict__ res, u64 one,"
+             " float* ring, int lane, long long first, long long stride) {\n"
+          << "  const long long G = (N + " << kCols - 1 << ") / " << kCols << ";\n"
+          << "  const long long ng = first < G ? (G - first + stride - 1) / stride : 0;\n"
+          << "  long long ig = 0; int ikc = 0; bool valid = false; const float* src = nullptr;\n"
+          << "  auto set_src = [&](long long gi) {\n"
+          << "    const long long nq = (first + gi * stride) * " << kCols << " + 4 * (lane & 15);\n"
+          << "    valid = gi < ng && nq < N;\n"
+          << "    if (valid) { const long long b = nq / S, s = nq - b * S;"
+             " src = act + b * K * S + s + (lane >> 4) * S; }\n"
+          << "  };\n"
+          << "  const unsigned ring_sa = sa(ring);\n"
+          << "  int islot = 0, cslot = 0;\n"
+          << "  auto issue = [&]() {\n"
+          << "    const unsigned dst = ring_sa + islot * (KC * " << kCols * 4 << ") + ((lane >> 4) * "
+          << kCols << " + 4 * (lane & 15)) * 4;\n"
+          << "    if (valid) {\n"
+          << "      const float* sk = src + (long long)ikc * KC * S;\n";
+        for (int j = 0; j < kKC / 2; ++j) {
+            const std::string cp = "CP16(dst, " + std::to_string(2 * j * kCols * 4) + ", sk + " +
+                                   std::to_string(2 * j) + "LL * S);";
+            if (K % kKC == 0)
+                o << "      " << cp << "\n";
+            else
+                o << "      if (ikc * KC + (lane >> 4) + " << 2 * j << " < K) " << cp << "\n";
+        }
+        o << "    }\n"
+          << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n"
+          << "    if (++islot == P) islot = 0;\n"
+          << "    if (++ikc == NKC) { ikc = 0; ++ig; set_src(ig); }\n"
+          << "  };\n"
+          << "  set_src(0);\n"
+          << "#pragma unroll 1\n"
+          << "  for (int p = 0; p < P - 1; ++p) issue();\n"
+          << "#pragma unroll 1\n"
+          << "  for (long long gi = 0; gi < ng; ++gi) {\n";
+        for (int q = 0; q < R; ++q) {
+            const int r = sg.r0 + q;
+            o << "    u64 a" << q << " = " << (key.bias ? "dup(__ldg(bias + " + std::to_string(r) + "))" : "0ULL")
+              << ";\n";
+        }
+        for (int kc = 0; kc < nkc; ++kc) {
+            o << "    issue();\n"
+              << "    asm volatile(\"cp.async.wait_group %0;\" :: \"n\"(P - 1) : \"memory\");\n"
+              << "    __syncwarp();\n"
+              << "    { const unsigned xs = ring_sa + cslot * (KC * " << kCols * 4 << ") + 8 * lane;\n";
+            for (int k = kc * kKC; k < std::min(K, (kc + 1) * kKC); ++k) {
+                if (by_k[k].empty()) continue;
+                o << "      { u64 x; LDS64(x, xs, " << (k - kc * kKC) * kCols * 4 << ");\n";
+                for (const auto& [q, v] : by_k[k]) {
+                    if (key.strict)
+                        o << "        a" << q << " = fma2(a" << q << ", one, mul2(" << imm2(v) << ", x));\n";
+                    else
+                        o << "        a" << q << " = fma2(" << imm2(v) << ", x, a" << q << ");\n";
+                }
+                o << "      }\n";
+            }
+            o << "    }\n    __syncwarp();\n    if (++cslot == P) cslot = 0;\n";
+        }
+        o << "    const long long n0 = (first + gi * stride) * " << kCols << " + 2 * lane;\n"
+          << "    if (n0 < N) {\n"
+          << "      const long long b = n0 / S, s = n0 - b * S;\n"
+          << "      const int S2 = (int)(S >> 1);\n"
+          << "      float2* op = reinterpret_cast<float2*>(out + (b * " << key.m_out << "LL + " << sg.r0
+          << ") * S + s);\n";
+        if (key.res)
+            o << "      const float2* rp = reinterpret_cast<const float2*>(res + (b * " << key.m_out
+              << "LL + " << sg.r0 << ") * S + s);\n";
+        for (int q = 0; q < R; ++q) {
+            o << "      { float2 v = make_float2(lo32(a" << q << "), hi32(a" << q << "));\n";
+            if (key.clamp) o << "        v.x = clampf(v.x, lo, hi); v.y = clampf(v.y, lo, hi);\n";
+            if (key.res)
+                o << "        { const float2 t = __ldcs(rp); rp += S2;"
+                     " v.x = __fadd_rn(v.x, t.x); v.y = __fadd_rn(v.y, t.y); }\n";
+            o << "        __stcs(op, v); op += S2; }  // row " << sg.r0 + q << "\n";
+        }
+        o << "    }\n  }\n}\n";
+    }
+    o << "extern \"C\" __global__ void __launch_bounds__(W * 32, 1)"
+         " spcv_jit(const float* __restrict__ act, float* __restrict__ out,"
+         " const float* __restrict__ bias, long long N, long long S, float lo, float hi,"
+         " const float* __restrict__ res, u64 one) {\n"
+      << "  extern __shared__ float4 smem4[];\n"
+      << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+      << "  float* ring = reinterpret_cast<float*>(smem4) + warp * (P * KC * " << kCols << ");\n"
+      << "  const int seg = seg_of[blockIdx.x], rank = rank_of[blockIdx.x];\n"
+      << "  switch (seg) {\n";
+    for (size_t si = 0; si < segs.size(); ++si)
+        o << "    case " << si << ": seg" << si << "(act, out, bias, N, S, lo, hi, res, one, ring, lane, "
+          << "(long long)rank * W + warp, " << segs[si].ctas * kJitWarps << "LL); break;\n";
     o << "  }\n}\n";
     return o.str();
 }
 
 std::mutex g_jit_mu;
 
-int jit_instr_budget() {
-    static const int b = [] {
-        const char* e = std::getenv("SPCV_JIT_MAX_INSTR");
-        return e ? std::atoi(e) : kJitMaxInstr;
-    }();
-    return b;
-}
-
-// Straight-line instructions per group: 2 (strict) or 1 (fast) per stored
-// weight of a stored row, one shared load per channel, ~6 per row (bias,
-// clamp, address, store).
-long long jit_instr_estimate(int M, int BH, const uint32_t* row_ptr, int K, const JitKey& key) {
-    long long weights = 0;
-    for (int r = 0; r < std::min(M, key.m_out); ++r)
-        weights += row_ptr[r / BH + 1] - row_ptr[r / BH];
-    return (key.strict ? 2 : 1) * weights + K + 6LL * std::min(M, key.m_out);
-}
-
 }  // namespace
 
-// Compile (once per weights x mode) and cache in the weights object.
 namespace spcv_detail {
 
 // NVRTC: source -> sm_100a cubin. No device needed.
@@ -190,8 +276,6 @@ int jit_compile(const std::string& src, std::vector<char>& cubin) {
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), "spcv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
         return fail(SPCV_ERR_UNSUPPORTED, "jit: nvrtcCreateProgram failed");
-    // --fmad=false: strict kernels must keep FMUL and FADD separate (fast ones
-    // use explicit __fmaf_rn, unaffected).
     const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false"};
     if (nvrtcCompileProgram(prog, 3, opts) != NVRTC_SUCCESS) {
         size_t n = 0;
@@ -216,12 +300,12 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     w->jit.emplace_back();
     JitVariant& v = w->jit.back();
     v.key = key;
-    if (jit_instr_estimate(w->rows, w->block_h, w->h_row_ptr.data(), w->cols, key) > jit_instr_budget())
-        return nullptr;  // too much straight-line code: the tile kernel runs
+    std::vector<Segment> segs;
+    if (!key.vec || !plan_segments(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), key, segs))
+        return nullptr;  // the tile kernel runs
     std::vector<char> cubin;
     const std::string src = gen_source(w->rows, w->cols, w->block_h, w->h_row_ptr.data(),
-                                       w->h_col_idx.data(), w->h_col_idx.size(),
-                                       w->h_values.data(), key);
+                                       w->h_col_idx.data(), w->h_values.data(), key, segs);
     if (jit_compile(src, cubin) != SPCV_OK) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&v.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
@@ -230,27 +314,17 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
         return nullptr;
     }
     e = cudaLibraryGetKernel(&v.fn, v.lib, "spcv_jit");
-    if (e != cudaSuccess) {
-        cuda_fail(e, "jit: cudaLibraryGetKernel");
-        cudaLibraryUnload(v.lib);
-        v.lib = nullptr;
-        v.fn = nullptr;
-        return nullptr;
-    }
-    const JitGeometry geo = jit_geometry(w->cols);
-    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, geo.smem);
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v.blocks_per_sm,
-                                                          reinterpret_cast<const void*>(v.fn),
-                                                          geo.warps * 32, geo.smem);
-    if (e != cudaSuccess || v.blocks_per_sm < 1) {
-        cuda_fail(e, "jit: kernel attributes");
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, jit_smem_bytes());
+    if (e != cudaSuccess) {
+        cuda_fail(e, "jit: kernel setup");
         cudaLibraryUnload(v.lib);
         v.lib = nullptr;
         v.fn = nullptr;
         return nullptr;
     }
+    v.segments = static_cast<int>(segs.size());
     return &v;
 }
 
@@ -260,35 +334,34 @@ void jit_release(spcv_cu_weights* w) {
     w->jit.clear();
 }
 
-int jit_launch(const JitVariant* v, int K, int sms, const spcvk::KernelArgs& a, cudaStream_t st) {
-    // persistent: one wave of resident CTAs, rounds of W groups of 32 columns
-    const JitGeometry geo = jit_geometry(K);
-    const long long groups = (a.N + 31) / 32;
-    const long long want = (groups + geo.warps - 1) / geo.warps;
-    const long long blocks = std::min<long long>(want, static_cast<long long>(v->blocks_per_sm) * sms);
+int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st) {
     long long N = a.N, S = a.S;
     float lo = a.lo, hi = a.hi;
     const float* act = a.act;
     float* out = a.out;
     const float* bias = a.bias;
     const float* res = a.residual;
-    void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res};
-    SPCV_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->fn), dim3(static_cast<unsigned>(blocks)),
-                               dim3(geo.warps * 32), args, geo.smem, st));
+    unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
+    void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res, &one};
+    SPCV_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->fn), dim3(v->key.sms),
+                               dim3(kJitWarps * 32), args, jit_smem_bytes(), st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }
 
 }  // namespace spcv_detail
 
-// Test hook (not in the public header): generate and compile the specialised
-// kernel for a host BCSR matrix without a device; reports the source and cubin
-// sizes and, when src_out is non-null, copies up to src_cap bytes of source.
+// Test hook (not in the public header): plan, generate and compile the
+// specialised kernel for a host BCSR matrix without a device. Reports the
+// number of row segments, source and cubin sizes, and copies up to src_cap
+// bytes of source when src_out is non-null. Returns SPCV_ERR_UNSUPPORTED when
+// the matrix is not eligible (too many segments).
 extern "C" int spcvx_jit_compile(int rows, int cols, int block_h, const uint32_t* row_ptr,
                                  const uint32_t* col_idx, size_t nblocks, const float* values,
                                  int mode, int act_kind, int has_bias, int has_res, int m_out,
-                                 size_t* src_bytes, size_t* cubin_bytes, char* src_out,
-                                 size_t src_cap) {
+                                 int sms, int* segments, size_t* src_bytes, size_t* cubin_bytes,
+                                 char* src_out, size_t src_cap) {
+    (void)nblocks;
     JitKey key;
     key.strict = mode == SPCV_MODE_STRICT;
     key.clamp = act_kind == SPCV_ACT_CLAMP;
@@ -296,7 +369,11 @@ extern "C" int spcvx_jit_compile(int rows, int cols, int block_h, const uint32_t
     key.res = has_res != 0;
     key.m_out = m_out;
     key.vec = true;
-    const std::string src = gen_source(rows, cols, block_h, row_ptr, col_idx, nblocks, values, key);
+    key.sms = sms;
+    std::vector<Segment> segs;
+    if (!plan_segments(rows, cols, block_h, row_ptr, key, segs)) return SPCV_ERR_UNSUPPORTED;
+    if (segments) *segments = static_cast<int>(segs.size());
+    const std::string src = gen_source(rows, cols, block_h, row_ptr, col_idx, values, key, segs);
     if (src_bytes) *src_bytes = src.size();
     if (src_out && src_cap) {
         const size_t n = std::min(src_cap - 1, src.size());

@@ -322,7 +322,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     {
         const char* e = std::getenv("SPCV_JIT");
         const bool off = e && std::atoi(e) == 0;
-        w->jit_eligible = !off && cols <= kJitMaxK && nvalues <= kJitMaxWeights;
+        w->jit_eligible = !off && nvalues <= kJitMaxWeights;
         if (w->jit_eligible) {
             w->h_row_ptr.assign(row_ptr, row_ptr + brows + 1);
             w->h_col_idx.assign(col_idx, col_idx + nblocks);
@@ -404,6 +404,7 @@ extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel)
         key.bias = true;
         key.vec = true;
         key.m_out = w->rows;
+        key.sms = props_for(w->device).sms;
         if (jit_prepare(w, key)) *kernel = SPCV_KERNEL_JIT;
         cudaSetDevice(prev);
     }
@@ -489,10 +490,13 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
         key.clamp = act_kind == SPCV_ACT_CLAMP;
         key.bias = bias != nullptr;
         key.res = residual != nullptr;
-        key.vec = S % 4 == 0 && reinterpret_cast<uintptr_t>(act) % 16 == 0;
+        key.vec = S % 4 == 0 && reinterpret_cast<uintptr_t>(act) % 16 == 0 &&
+                  reinterpret_cast<uintptr_t>(out) % 8 == 0 &&
+                  reinterpret_cast<uintptr_t>(residual) % 8 == 0;
         key.m_out = a.M_out;
+        key.sms = sms;
         if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key))
-            return jit_launch(v, w->cols, sms, a, st);
+            return jit_launch(v, a, st);
     }
     switch (w->block_h) {
         case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);

@@ -14,21 +14,23 @@
 #include "spmm_kernel.cuh"
 
 // A weight-specialised kernel compiled at run time (jit.cu), one per call
-// shape: arithmetic mode, activation kind, bias/residual presence, stored rows.
+// shape: arithmetic mode, activation kind, bias/residual presence, stored
+// rows, 16 B-vectorisable activations, SM count of the device.
 struct JitKey {
     bool strict = true, clamp = false, bias = false, res = false;
-    bool vec = false;  // S % 4 == 0 and 16 B aligned activations: 16 B copies
+    bool vec = false;  // S % 4 == 0 and 16 B aligned activations / 8 B aligned outputs
     int m_out = 0;
+    int sms = 0;
     bool operator==(const JitKey& o) const {
         return strict == o.strict && clamp == o.clamp && bias == o.bias && res == o.res &&
-               vec == o.vec && m_out == o.m_out;
+               vec == o.vec && m_out == o.m_out && sms == o.sms;
     }
 };
 struct JitVariant {
     JitKey key;
     cudaLibrary_t lib = nullptr;
-    cudaKernel_t fn = nullptr;  // null: not built (over budget, or compile/load failed)
-    int blocks_per_sm = 0;
+    cudaKernel_t fn = nullptr;  // null: not built (ineligible, or compile/load failed)
+    int segments = 0;
 };
 
 struct spcv_cu_weights {
@@ -79,23 +81,16 @@ int launch_bh2(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
 int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntiles, int sms,
                bool strict, bool vec, cudaStream_t);
 
-// Weight-specialised kernels for small K (jit.cu).
-constexpr int kJitMaxK = 128;             // activation registers per thread
-constexpr size_t kJitMaxWeights = 16384;  // host copy kept for matrices up to this size
-constexpr int kJitMaxInstr = 4608;        // straight-line code budget (instruction cache)
-// One CTA per SM: W warps, P prefetch stages of a [K][32] fp32 slot per warp.
-struct JitGeometry {
-    int warps, stages, smem;
-};
-inline JitGeometry jit_geometry(int K) {
-    const int slot = K * 32 * 4;
-    int warps = K <= 64 ? 16 : 12;
-    int stages = 1;
-    while (stages < 3 && warps * slot * (stages + 1) <= 200 * 1024) ++stages;
-    return {warps, stages, warps * slot * stages};
-}
+// Weight-specialised kernels (jit.cu): one persistent CTA of kJitWarps warps
+// per SM, a kJitStages-deep ring of [32 channels][64 columns] fp32 per warp.
+constexpr size_t kJitMaxWeights = size_t(1) << 21;  // host copy kept up to this many values
+constexpr int kJitSegInstr = 5000;  // straight-line instructions per row segment (i-cache)
+constexpr int kJitMaxSegs = 2;      // segments per matrix (more: i-cache misses, L2 re-reads)
+constexpr int kJitWarps = 8;
+constexpr int kJitStages = 3;
+inline int jit_smem_bytes() { return kJitWarps * kJitStages * 32 * 64 * 4; }
 const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
-int jit_launch(const JitVariant* v, int K, int sms, const spcvk::KernelArgs& a, cudaStream_t st);
+int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st);
 void jit_release(spcv_cu_weights* w);
 
 }  // namespace spcv_detail

@@ -502,21 +502,26 @@ JIT_CASES = [
     ("pw1", mbv1_pointwise()[0], 2),
     ("pw2", mbv1_pointwise()[1], 1),
     ("pw3", mbv1_pointwise()[2], 1),
-    ("bh2_odd", Layer("b2", 96, 64, 7, 9, ("clamp", 0.0, 6.0), -1.0, 1.0, 0.8, 2), 5),
-    ("bh4_none", Layer("b4", 128, 128, 5, 5, ("none", 0.0, 0.0), -1.0, 1.0, 0.9, 4), 4),
-    ("k1", Layer("k1", 1, 8, 3, 3, ("none", 0.0, 0.0), -1.0, 1.0, 0.0), 2),
+    ("pw4", mbv1_pointwise()[3], 2),
+    ("bh2_tail", Layer("b2", 96, 64, 8, 9, ("clamp", 0.0, 6.0), -1.0, 1.0, 0.8, 2), 5),
+    ("bh4_none", Layer("b4", 128, 128, 4, 6, ("none", 0.0, 0.0), -1.0, 1.0, 0.9, 4), 4),
+    ("k1", Layer("k1", 1, 8, 4, 4, ("none", 0.0, 0.0), -1.0, 1.0, 0.0), 2),
+    ("k33_partial_chunk", Layer("k33", 33, 40, 4, 5, sparsity=0.5), 3),
     ("dense", Layer("d", 16, 32, 4, 4, sparsity=0.0), 2),
-    ("empty_rows", Layer("e", 32, 40, 3, 5, ("clamp", -0.5, 0.5), -1.0, 1.0, 0.97), 3),
+    ("empty_rows", Layer("e", 32, 40, 4, 5, ("clamp", -0.5, 0.5), -1.0, 1.0, 0.97), 3),
 ]
 
 
 @pytest.mark.parametrize("kernel", ["jit", "tile"])
 @pytest.mark.parametrize("case", JIT_CASES, ids=lambda c: c[0])
 def test_jit_and_tile_small_k_bit_exact(oracle, monkeypatch, kernel, case):
-    """K <= 128: the weight-specialised kernel (SPCV_JIT default) and the tile
-    kernel (SPCV_JIT=0) both equal the oracle bit-for-bit in strict mode, with
-    and without bias, and stay within the fast-mode bound."""
+    """The weight-specialised kernel (SPCV_JIT default) and the tile kernel
+    (SPCV_JIT=0) both equal the oracle bit-for-bit in strict mode, with and
+    without bias, and stay within the fast-mode bound (S % 4 == 0 cases: the
+    JIT kernel's 16 B staging; column tails, partial channel chunks, empty
+    rows and one-channel matrices included)."""
     monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    monkeypatch.setenv("SPCV_JIT_MAX_SEGS", "48")  # exercise multi-segment plans too
     _, layer, images = case
     d = make_layer_data(layer, images, 99)
     dw = sp.DeviceBcsr(d.weights)
@@ -532,13 +537,23 @@ def test_jit_and_tile_small_k_bit_exact(oracle, monkeypatch, kernel, case):
 
 def test_jit_not_used_beyond_its_limits(monkeypatch):
     monkeypatch.delenv("SPCV_JIT", raising=False)
-    big_k = make_layer_data(Layer("k", 129, 8, 2, 2, sparsity=0.5), 1, 1)
-    assert sp.DeviceBcsr(big_k.weights).kernel() == "tile"
-    small = make_layer_data(Layer("s", 128, 8, 2, 2, sparsity=0.5), 1, 1)
+    monkeypatch.delenv("SPCV_JIT_MAX_SEGS", raising=False)
+    monkeypatch.delenv("SPCV_JIT_SEG_INSTR", raising=False)
+    small = make_layer_data(Layer("s", 300, 8, 2, 2, sparsity=0.5), 1, 1)
     assert sp.DeviceBcsr(small.weights).kernel() == "jit"
-    # MBv1 pw4 (3.3k weights): over the straight-line code budget in both modes
-    pw4 = sp.DeviceBcsr(make_layer_data(mbv1_pointwise()[3], 1, 1).weights)
-    assert pw4.kernel(strict=True) == "tile" and pw4.kernel(strict=False) == "tile"
+    # half-dense 1024 x 1024: far more row segments than the cap -> tile kernel
+    big = make_layer_data(Layer("b", 1024, 1024, 2, 2, sparsity=0.5), 1, 1)
+    assert sp.DeviceBcsr(big.weights).kernel() == "tile"
+
+
+def test_jit_odd_spatial_falls_back_to_tile_bit_exact(oracle):
+    """S % 4 != 0 (or unaligned buffers) cannot use the 16 B staging: the call
+    runs the tile kernel and stays bit-exact."""
+    layer = Layer("odd", 64, 48, 7, 7, sparsity=0.8)
+    d = make_layer_data(layer, 3, 5)
+    got = run_device(d.weights, d.act, d.bias, layer.act)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
 
 
 # ------------------------------------------------- dense fp32 baseline (§8f-1)

@@ -51,45 +51,74 @@ def _jit_compile(m, mode, act_kind=1, has_bias=1, has_res=0, m_out=None):
     lib = ctypes.CDLL(os.path.join(LIBDIR, "libspcv_cu.so"))
     fn = lib.spcvx_jit_compile
     P, Z, I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
-    fn.argtypes = [I, I, I, P, P, Z, P, I, I, I, I, I, ctypes.POINTER(Z), ctypes.POINTER(Z),
-                   ctypes.c_char_p, Z]
+    fn.argtypes = [I, I, I, P, P, Z, P, I, I, I, I, I, I, ctypes.POINTER(I), ctypes.POINTER(Z),
+                   ctypes.POINTER(Z), ctypes.c_char_p, Z]
     rp = np.ascontiguousarray(m.row_ptr, np.uint32)
     ci = np.ascontiguousarray(m.col_idx, np.uint32)
     va = np.ascontiguousarray(m.values, np.float32)
-    sb, cb = Z(), Z()
+    sb, cb, nseg = Z(), Z(), I()
     buf = ctypes.create_string_buffer(1 << 20)
     rc = fn(m.rows, m.cols, m.block_h, rp.ctypes.data, ci.ctypes.data if ci.size else None, ci.size,
             va.ctypes.data if va.size else None, mode, act_kind, has_bias, has_res,
-            m.rows if m_out is None else m_out, ctypes.byref(sb), ctypes.byref(cb), buf, 1 << 20)
-    return rc, buf.value.decode(), cb.value
+            m.rows if m_out is None else m_out, 148, ctypes.byref(nseg), ctypes.byref(sb),
+            ctypes.byref(cb), buf, 1 << 20)
+    return rc, buf.value.decode(), cb.value, nseg.value
 
 
-def test_jit_kernel_source_and_nvrtc_compile_without_gpu():
-    """The small-K kernel (jit.cu) is generated from the matrix and compiled by
-    NVRTC for sm_100a; neither step needs a device. Every stored weight appears
-    once per row as an exact hex-float immediate, in ascending column order."""
+def _jit_terms(src):
+    """(segment, accumulator) -> [(channel, weight bits, op)] in program order,
+    parsed from the generated k-major source (chunk = one issue() per 32 channels)."""
+    terms, seg, kc = {}, -1, -1
+    for line in src.splitlines():
+        m = re.match(r"__device__ __forceinline__ void seg(\d+)\(", line)
+        if m:
+            seg, kc = int(m.group(1)), -1
+            continue
+        if line.strip() == "issue();":
+            kc += 1
+        m = re.search(r"LDS64\(x, xs, (\d+)\)", line)
+        if m:
+            k = kc * 32 + int(m.group(1)) // 256
+        m = re.search(r"a(\d+) = fma2\(a\d+, one, mul2\(0x([0-9a-f]{8})[0-9a-f]{8}ULL, x\)\)", line)
+        if m:
+            terms.setdefault((seg, int(m.group(1))), []).append((k, int(m.group(2), 16), "strict"))
+        m = re.search(r"a(\d+) = fma2\(0x([0-9a-f]{8})[0-9a-f]{8}ULL, x, a\d+\)", line)
+        if m:
+            terms.setdefault((seg, int(m.group(1))), []).append((k, int(m.group(2), 16), "fast"))
+    return terms
+
+
+def test_jit_kernel_source_and_nvrtc_compile_without_gpu(monkeypatch):
+    """The weight-specialised kernel (jit.cu) is planned, generated and compiled
+    by NVRTC for sm_100a without a device. Every stored weight of every row
+    (zeros inside stored blocks included) appears exactly once as an immediate,
+    in ascending channel order, split over row segments that cover the rows."""
+    monkeypatch.setenv("SPCV_JIT_SEG_INSTR", "200")  # force several segments
     rng = np.random.default_rng(3)
-    dense = rng.standard_normal((12, 20)).astype(np.float32)
-    dense[rng.random((12, 20)) < 0.7] = 0
+    dense = rng.standard_normal((12, 70)).astype(np.float32)
+    dense[rng.random((12, 70)) < 0.7] = 0
     m = sp.encode_bcsr(dense, 2)
-    rc, src, cubin = _jit_compile(m, _capi.MODE_STRICT)
-    assert rc == 0 and cubin > 0
-    assert src.count("__fmul_rn(") == m.nnz_values() and "__fmaf_rn" not in src
     rp, ci, va = np.asarray(m.row_ptr), np.asarray(m.col_idx), np.asarray(m.values)
-    for r in range(12):  # stored blocks of r's block row, zeros inside blocks included
-        blks = range(rp[r // 2], rp[r // 2 + 1])
-        body = src.split("__stcs(o + %dLL * S" % r)[0].rsplit("{", 1)[1]
-        imms = re.findall(r"__fmul_rn\(\(?([^,()]*)\)?, x(\d+)\)", body)
-        assert [int(k) for _, k in imms] == [int(ci[b]) for b in blks]
-        got = np.array([float.fromhex(v.rstrip("f")) if "0x" in v else float(v.rstrip("f"))
-                        for v, _ in imms], np.float32)
-        want = np.array([va[2 * b + r % 2] for b in blks], np.float32)
-        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
-    rc, src, _ = _jit_compile(m, _capi.MODE_FAST, act_kind=0, has_bias=0, has_res=1, m_out=11)
-    assert rc == 0
-    assert src.count("__fmaf_rn(") == sum(2 * (rp[i + 1] - rp[i]) for i in range(5)) + rp[6] - rp[5]
-    assert "lo ?" not in src
-    assert "__stcs(o + 11LL" not in src and "__ldcs(r + 10LL" in src
+    for mode, m_out in ((_capi.MODE_STRICT, 12), (_capi.MODE_FAST, 11)):
+        rc, src, cubin, nseg = _jit_compile(m, mode, m_out=m_out)
+        assert rc == 0 and cubin > 0 and nseg > 1
+        terms = _jit_terms(src)
+        rows = []
+        for seg in range(nseg):
+            body = src.split("void seg%d(" % seg)[1].split("__device__")[0]
+            rows += [int(r) for r in re.findall(r"// row (\d+)", body)]
+        assert rows == list(range(m_out))  # segments partition the stored rows, in order
+        r = 0
+        for seg in range(nseg):
+            q = 0
+            while (seg, q) in terms or (r < m_out and rp[r // 2] == rp[r // 2 + 1]):
+                blks = range(rp[r // 2], rp[r // 2 + 1])
+                want = [(int(ci[b]), int(va[2 * b + r % 2].view(np.uint32)),
+                         "strict" if mode == _capi.MODE_STRICT else "fast") for b in blks]
+                assert terms.get((seg, q), []) == want, (seg, q, r)
+                q += 1
+                r += 1
+        assert r == m_out
 
 
 def test_cpp_dropin_library_exports_reference_api():

@@ -38,6 +38,10 @@ def run_layer(args, cfg, li, L, name):
     images = args.images or cfg["images"]
     d = make_layer_data(L, images, 1000 * (li + 1))
     dw = sp.DeviceBcsr(d.weights)
+    import time
+    t0 = time.time()
+    kern = dw.kernel(args.mode == "strict")
+    prep = time.time() - t0
     a = torch.from_numpy(d.act).cuda()
     b = torch.from_numpy(d.bias).cuda()
     o = torch.empty(images, L.cout, L.h, L.w, device="cuda")
@@ -55,7 +59,7 @@ def run_layer(args, cfg, li, L, name):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     us = statistics.median(ts)
-    print(f"{name} kernel={dw.kernel(args.mode == 'strict')} K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
+    print(f"{name} kernel={kern} (prep {prep:.1f}s) K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
           f"median {us:.1f} us  {d.flops() / us / 1e3:.0f} GFLOP/s  {d.alg_bytes() / us / 1e3:.0f} GB/s "
           f"(alg bytes {d.alg_bytes():.0f})")
 
