@@ -50,6 +50,13 @@ constexpr int kKC = 32;        // channels per staged chunk
 constexpr int kCols = 64;      // columns per warp group (2 per lane)
 constexpr int kRowsMax = 64;   // rows per segment (2 accumulator registers each)
 
+// Rows a segment may hold so that its accumulator pairs fit the register
+// budget of a W-warp CTA (65536 / (32 W), at most 255) with ~48 to spare.
+int rows_max(int warps) {
+    const int regs = std::min(255, 65536 / (32 * warps));
+    return std::max(8, std::min(kRowsMax, (regs - 48) / 2));
+}
+
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -89,7 +96,7 @@ bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& 
     cur.instr = fixed;
     for (int r = 0; r < rows; ++r) {
         const long long c = static_cast<long long>(per_weight) * row_nnz(row_ptr, BH, r) + 10;
-        if (cur.r1 > cur.r0 && (cur.instr + c > budget || cur.r1 - cur.r0 == kRowsMax)) {
+        if (cur.r1 > cur.r0 && (cur.instr + c > budget || cur.r1 - cur.r0 == rows_max(key.warps))) {
             segs.push_back(cur);
             cur = Segment();
             cur.r0 = cur.r1 = r;
@@ -132,7 +139,7 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
     const int nkc = (K + kKC - 1) / kKC;
     std::ostringstream o;
     o << "#define K " << K << "LL\n#define KC " << kKC << "\n#define NKC " << nkc
-      << "\n#define W " << kJitWarps << "\n#define P " << kJitStages << "\n"
+      << "\n#define W " << key.warps << "\n#define P " << key.stages << "\n"
       << "typedef unsigned long long u64;\n"
       << "__device__ __forceinline__ unsigned sa(const void* p) {"
          " return (unsigned)__cvta_generic_to_shared(p); }\n"
@@ -260,9 +267,92 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
       << "  switch (seg) {\n";
     for (size_t si = 0; si < segs.size(); ++si)
         o << "    case " << si << ": seg" << si << "(act, out, bias, N, S, lo, hi, res, one, ring, lane, "
-          << "(long long)rank * W + warp, " << segs[si].ctas * kJitWarps << "LL); break;\n";
+          << "(long long)rank * W + warp, " << segs[si].ctas * key.warps << "LL); break;\n";
     o << "  }\n}\n";
     return o.str();
+}
+
+// Direct variant for small K (<= kJitDirectMaxK): one thread per virtual
+// column, 128-thread CTAs, no shared memory and no layout requirement. The
+// thread loads its column's activations straight into registers (coalesced
+// across the warp), then every row is straight-line code with the weights as
+// immediates, 4 rows interleaved term by term; per row the order is the
+// reference's (bias first, blocks ascending).
+long long direct_instr(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key) {
+    long long weights = 0;
+    const int rows = std::min(M, key.m_out);
+    for (int r = 0; r < rows; ++r) weights += row_nnz(row_ptr, BH, r);
+    return (key.strict ? 2 : 1) * weights + K + 6LL * rows;
+}
+
+std::string gen_direct(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
+                       const float* values, const JitKey& key) {
+    std::ostringstream o;
+    o << "extern \"C\" __global__ void __launch_bounds__(128) spcv_jit(const float* __restrict__ act,"
+         " float* __restrict__ out, const float* __restrict__ bias, long long N, long long S,"
+         " float lo, float hi, const float* __restrict__ res, unsigned long long one) {\n"
+      << "  const long long n = blockIdx.x * 128LL + threadIdx.x;\n"
+      << "  if (n >= N) return;\n"
+      << "  const long long b = n / S, s = n - b * S;\n"
+      << "  const float* a = act + b * " << K << "LL * S + s;\n"
+      << "  float* o = out + b * " << key.m_out << "LL * S + s;\n";
+    if (key.res) o << "  const float* rp = res + b * " << key.m_out << "LL * S + s;\n";
+    std::vector<char> used(static_cast<size_t>(K), 0);
+    const int brows = M / BH;
+    for (uint32_t b = 0; b < row_ptr[brows]; ++b) used[col_idx[b]] = 1;
+    for (int k = 0; k < K; ++k)
+        if (used[k]) o << "  const float x" << k << " = __ldcs(a + " << k << "LL * S);\n";
+    constexpr int kIL = 4;
+    const int rows = std::min(M, key.m_out);
+    for (int r0 = 0; r0 < rows; r0 += kIL) {
+        const int r1 = std::min(rows, r0 + kIL);
+        o << "  {\n";
+        int longest = 0;
+        for (int r = r0; r < r1; ++r) {
+            longest = std::max(longest, row_nnz(row_ptr, BH, r));
+            o << "    float a" << r - r0 << " = "
+              << (key.bias ? "__ldg(bias + " + std::to_string(r) + ")" : "0.0f") << ";\n";
+        }
+        for (int t = 0; t < longest; ++t) {
+            for (int r = r0; r < r1; ++r) {
+                if (t >= row_nnz(row_ptr, BH, r)) continue;
+                const uint32_t blk = row_ptr[r / BH] + static_cast<uint32_t>(t);
+                const std::string A = "a" + std::to_string(r - r0);
+                float v = values[static_cast<size_t>(blk) * BH + r % BH];
+                uint32_t u;
+                std::memcpy(&u, &v, 4);
+                char wv[40];
+                std::snprintf(wv, sizeof wv, "__uint_as_float(0x%08xu)", u);
+                const std::string x = "x" + std::to_string(col_idx[blk]);
+                if (key.strict)
+                    o << "    " << A << " = __fadd_rn(" << A << ", __fmul_rn(" << wv << ", " << x << "));\n";
+                else
+                    o << "    " << A << " = __fmaf_rn(" << wv << ", " << x << ", " << A << ");\n";
+            }
+        }
+        for (int r = r0; r < r1; ++r) {
+            const std::string A = "a" + std::to_string(r - r0);
+            if (key.clamp)
+                o << "    " << A << " = " << A << " < lo ? lo : (" << A << " > hi ? hi : " << A << ");\n";
+            if (key.res) o << "    " << A << " = __fadd_rn(" << A << ", __ldcs(rp + " << r << "LL * S));\n";
+            o << "    __stcs(o + " << r << "LL * S, " << A << ");  // row " << r << "\n";
+        }
+        o << "  }\n";
+    }
+    o << "}\n";
+    return o.str();
+}
+
+// Which generator serves (matrix, key): direct for small K within the code
+// budget, else the k-major segmented kernel when the layout allows it.
+enum class JitKind { kNone, kDirect, kKMajor };
+JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key,
+                    std::vector<Segment>& segs) {
+    if (K <= env_int("SPCV_JIT_DIRECT_MAXK", kJitDirectMaxK) &&
+        direct_instr(M, K, BH, row_ptr, key) <= env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr))
+        return JitKind::kDirect;
+    if (key.vec && plan_segments(M, K, BH, row_ptr, key, segs)) return JitKind::kKMajor;
+    return JitKind::kNone;
 }
 
 std::mutex g_jit_mu;
@@ -301,11 +391,15 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     JitVariant& v = w->jit.back();
     v.key = key;
     std::vector<Segment> segs;
-    if (!key.vec || !plan_segments(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), key, segs))
-        return nullptr;  // the tile kernel runs
+    const JitKind kind = choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), key, segs);
+    if (kind == JitKind::kNone) return nullptr;  // the tile kernel runs
+    v.direct = kind == JitKind::kDirect;
     std::vector<char> cubin;
-    const std::string src = gen_source(w->rows, w->cols, w->block_h, w->h_row_ptr.data(),
-                                       w->h_col_idx.data(), w->h_values.data(), key, segs);
+    const std::string src =
+        v.direct ? gen_direct(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
+                              w->h_values.data(), key)
+                 : gen_source(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
+                              w->h_values.data(), key, segs);
     if (jit_compile(src, cubin) != SPCV_OK) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&v.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
@@ -314,9 +408,10 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
         return nullptr;
     }
     e = cudaLibraryGetKernel(&v.fn, v.lib, "spcv_jit");
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && !v.direct)
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, jit_smem_bytes());
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 jit_smem_bytes(key.warps, key.stages));
     if (e != cudaSuccess) {
         cuda_fail(e, "jit: kernel setup");
         cudaLibraryUnload(v.lib);
@@ -326,6 +421,15 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     }
     v.segments = static_cast<int>(segs.size());
     return &v;
+}
+
+void jit_geometry(JitKey& key) {
+    key.warps = env_int("SPCV_JIT_WARPS", kJitWarps);
+    key.stages = env_int("SPCV_JIT_STAGES", kJitStages);
+    if (key.warps < 1 || key.warps > 32) key.warps = kJitWarps;
+    if (key.stages < 1 || key.stages > 8) key.stages = kJitStages;
+    while (key.stages > 1 && jit_smem_bytes(key.warps, key.stages) > 227 * 1024) --key.stages;
+    while (jit_smem_bytes(key.warps, key.stages) > 227 * 1024) --key.warps;
 }
 
 void jit_release(spcv_cu_weights* w) {
@@ -343,8 +447,17 @@ int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st)
     const float* res = a.residual;
     unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
     void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res, &one};
+    if (v->direct) {
+        const long long blocks = (N + 127) / 128;
+        if (blocks > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "jit: grid too large");
+        SPCV_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->fn),
+                                   dim3(static_cast<unsigned>(blocks)), dim3(128), args, 0, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return SPCV_OK;
+    }
     SPCV_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->fn), dim3(v->key.sms),
-                               dim3(kJitWarps * 32), args, jit_smem_bytes(), st));
+                               dim3(v->key.warps * 32), args,
+                               jit_smem_bytes(v->key.warps, v->key.stages), st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }
@@ -354,8 +467,8 @@ int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st)
 // Test hook (not in the public header): plan, generate and compile the
 // specialised kernel for a host BCSR matrix without a device. Reports the
 // number of row segments, source and cubin sizes, and copies up to src_cap
-// bytes of source when src_out is non-null. Returns SPCV_ERR_UNSUPPORTED when
-// the matrix is not eligible (too many segments).
+// bytes of source when src_out is non-null (segments = 0: direct variant).
+// Returns SPCV_ERR_UNSUPPORTED when the matrix is not eligible.
 extern "C" int spcvx_jit_compile(int rows, int cols, int block_h, const uint32_t* row_ptr,
                                  const uint32_t* col_idx, size_t nblocks, const float* values,
                                  int mode, int act_kind, int has_bias, int has_res, int m_out,
@@ -370,10 +483,14 @@ extern "C" int spcvx_jit_compile(int rows, int cols, int block_h, const uint32_t
     key.m_out = m_out;
     key.vec = true;
     key.sms = sms;
+    spcv_detail::jit_geometry(key);
     std::vector<Segment> segs;
-    if (!plan_segments(rows, cols, block_h, row_ptr, key, segs)) return SPCV_ERR_UNSUPPORTED;
-    if (segments) *segments = static_cast<int>(segs.size());
-    const std::string src = gen_source(rows, cols, block_h, row_ptr, col_idx, values, key, segs);
+    const JitKind kind = choose_kind(rows, cols, block_h, row_ptr, key, segs);
+    if (kind == JitKind::kNone) return SPCV_ERR_UNSUPPORTED;
+    if (segments) *segments = kind == JitKind::kDirect ? 0 : static_cast<int>(segs.size());
+    const std::string src = kind == JitKind::kDirect
+                                ? gen_direct(rows, cols, block_h, row_ptr, col_idx, values, key)
+                                : gen_source(rows, cols, block_h, row_ptr, col_idx, values, key, segs);
     if (src_bytes) *src_bytes = src.size();
     if (src_out && src_cap) {
         const size_t n = std::min(src_cap - 1, src.size());

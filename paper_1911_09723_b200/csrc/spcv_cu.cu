@@ -405,6 +405,7 @@ extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel)
         key.vec = true;
         key.m_out = w->rows;
         key.sms = props_for(w->device).sms;
+        jit_geometry(key);
         if (jit_prepare(w, key)) *kernel = SPCV_KERNEL_JIT;
         cudaSetDevice(prev);
     }
@@ -495,6 +496,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                   reinterpret_cast<uintptr_t>(residual) % 8 == 0;
         key.m_out = a.M_out;
         key.sms = sms;
+        jit_geometry(key);
         if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key))
             return jit_launch(v, a, st);
     }

@@ -21,15 +21,18 @@ struct JitKey {
     bool vec = false;  // S % 4 == 0 and 16 B aligned activations / 8 B aligned outputs
     int m_out = 0;
     int sms = 0;
+    int warps = 8, stages = 3;  // CTA geometry (jit_geometry)
     bool operator==(const JitKey& o) const {
         return strict == o.strict && clamp == o.clamp && bias == o.bias && res == o.res &&
-               vec == o.vec && m_out == o.m_out && sms == o.sms;
+               vec == o.vec && m_out == o.m_out && sms == o.sms && warps == o.warps &&
+               stages == o.stages;
     }
 };
 struct JitVariant {
     JitKey key;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t fn = nullptr;  // null: not built (ineligible, or compile/load failed)
+    bool direct = false;        // one thread per column (small K) vs k-major segments
     int segments = 0;
 };
 
@@ -86,9 +89,11 @@ int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
 constexpr size_t kJitMaxWeights = size_t(1) << 21;  // host copy kept up to this many values
 constexpr int kJitSegInstr = 5000;  // straight-line instructions per row segment (i-cache)
 constexpr int kJitMaxSegs = 2;      // segments per matrix (more: i-cache misses, L2 re-reads)
+constexpr int kJitDirectMaxK = 64;  // direct variant: activations of a column in registers
 constexpr int kJitWarps = 8;
 constexpr int kJitStages = 3;
-inline int jit_smem_bytes() { return kJitWarps * kJitStages * 32 * 64 * 4; }
+inline int jit_smem_bytes(int warps, int stages) { return warps * stages * 32 * 64 * 4; }
+void jit_geometry(JitKey& key);  // warps/stages (SPCV_JIT_WARPS / SPCV_JIT_STAGES override)
 const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
 int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st);
 void jit_release(spcv_cu_weights* w);

@@ -507,6 +507,8 @@ JIT_CASES = [
     ("bh4_none", Layer("b4", 128, 128, 4, 6, ("none", 0.0, 0.0), -1.0, 1.0, 0.9, 4), 4),
     ("k1", Layer("k1", 1, 8, 4, 4, ("none", 0.0, 0.0), -1.0, 1.0, 0.0), 2),
     ("k33_partial_chunk", Layer("k33", 33, 40, 4, 5, sparsity=0.5), 3),
+    ("k72_partial_chunk", Layer("k72", 72, 40, 4, 5, sparsity=0.5), 3),
+    ("direct_odd_spatial", Layer("odd", 48, 40, 7, 7, sparsity=0.8), 3),
     ("dense", Layer("d", 16, 32, 4, 4, sparsity=0.0), 2),
     ("empty_rows", Layer("e", 32, 40, 4, 5, ("clamp", -0.5, 0.5), -1.0, 1.0, 0.97), 3),
 ]
@@ -547,9 +549,9 @@ def test_jit_not_used_beyond_its_limits(monkeypatch):
 
 
 def test_jit_odd_spatial_falls_back_to_tile_bit_exact(oracle):
-    """S % 4 != 0 (or unaligned buffers) cannot use the 16 B staging: the call
-    runs the tile kernel and stays bit-exact."""
-    layer = Layer("odd", 64, 48, 7, 7, sparsity=0.8)
+    """S % 4 != 0 (or unaligned buffers) cannot use the k-major variant's 16 B
+    staging (K > 64): the call runs the tile kernel and stays bit-exact."""
+    layer = Layer("odd", 96, 48, 7, 7, sparsity=0.8)
     d = make_layer_data(layer, 3, 5)
     got = run_device(d.weights, d.act, d.bias, layer.act)
     want = oracle.spmm(d.weights, d.act, d.bias, layer.act).reshape(got.shape)

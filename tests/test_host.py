@@ -94,6 +94,7 @@ def test_jit_kernel_source_and_nvrtc_compile_without_gpu(monkeypatch):
     (zeros inside stored blocks included) appears exactly once as an immediate,
     in ascending channel order, split over row segments that cover the rows."""
     monkeypatch.setenv("SPCV_JIT_SEG_INSTR", "200")  # force several segments
+    monkeypatch.setenv("SPCV_JIT_MAX_SEGS", "48")
     rng = np.random.default_rng(3)
     dense = rng.standard_normal((12, 70)).astype(np.float32)
     dense[rng.random((12, 70)) < 0.7] = 0
@@ -119,6 +120,33 @@ def test_jit_kernel_source_and_nvrtc_compile_without_gpu(monkeypatch):
                 q += 1
                 r += 1
         assert r == m_out
+
+
+def test_jit_direct_variant_source(monkeypatch):
+    """Small K (<= 64): the direct variant (one thread per column). Each row's
+    terms appear in ascending channel order with the exact stored weights."""
+    monkeypatch.delenv("SPCV_JIT_SEG_INSTR", raising=False)
+    rng = np.random.default_rng(4)
+    dense = rng.standard_normal((10, 20)).astype(np.float32)
+    dense[rng.random((10, 20)) < 0.6] = 0
+    m = sp.encode_bcsr(dense, 1)
+    rp, ci, va = np.asarray(m.row_ptr), np.asarray(m.col_idx), np.asarray(m.values)
+    rc, src, cubin, nseg = _jit_compile(m, _capi.MODE_STRICT)
+    assert rc == 0 and cubin > 0 and nseg == 0
+    block, rows_seen = {}, []
+    for line in src.splitlines():
+        if line.strip() == "{":
+            block = {}
+        t = re.search(r"a(\d+) = __fadd_rn\(a\d+, __fmul_rn\(__uint_as_float\(0x([0-9a-f]{8})u\), x(\d+)\)\)", line)
+        if t:
+            block.setdefault(int(t.group(1)), []).append((int(t.group(3)), int(t.group(2), 16)))
+        st = re.search(r"__stcs\(o \+ (\d+)LL \* S, a(\d+)\);", line)
+        if st:
+            r = int(st.group(1))
+            rows_seen.append(r)
+            want = [(int(ci[b]), int(va[b].view(np.uint32))) for b in range(rp[r], rp[r + 1])]
+            assert block.get(int(st.group(2)), []) == want, r
+    assert rows_seen == list(range(10))
 
 
 def test_cpp_dropin_library_exports_reference_api():
