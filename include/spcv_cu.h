@@ -90,11 +90,15 @@ void spcv_cu_free(spcv_cu_weights* w);
 /* Which CUDA kernel spmm runs for these weights in `mode`:
  *   SPCV_KERNEL_TILE — the shared-memory tile kernel (any K up to the tile limit);
  *   SPCV_KERNEL_JIT  — a kernel specialised on this matrix's structure and
- *                      values (K <= 128 and <= 16384 stored weights), compiled
- *                      with NVRTC on first use and cached in the weights.
- * Compiles the specialised kernel if it is due and not built yet. Both kernels
- * are bit-exact in SPCV_MODE_STRICT. SPCV_JIT=0 in the environment at pack
- * time selects the tile kernel. No reference counterpart (introspection). */
+ *                      values (weights as instruction immediates), compiled
+ *                      with NVRTC on first use and cached in the weights:
+ *                      one thread per column for K <= 64, else k-major row
+ *                      segments (S % 4 == 0 layouts) while the code fits the
+ *                      instruction-cache budget (jit.cu).
+ * Compiles the specialised kernel if it is due and not built yet (probing the
+ * spmm_into call shape). Both kernels are bit-exact in SPCV_MODE_STRICT.
+ * SPCV_JIT=0 in the environment at pack time selects the tile kernel. No
+ * reference counterpart (introspection). */
 enum { SPCV_KERNEL_TILE = 0, SPCV_KERNEL_JIT = 1 };
 int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel);
 
@@ -178,6 +182,19 @@ int spcv_cu_model_weights(const spcv_cu_model* m, int i, const spcv_cu_weights**
  * layer has a residual source). act [images][cin][in_h*in_w] on device. */
 int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act, int images,
                       const float* residual, float* out, int mode, void* stream);
+
+/* The whole network (run_network, netdef.cpp:456-524) on the device: `images`
+ * HWC images input[images][in_h][in_w][in_c] (device memory) -> logits
+ * [images][num_classes] (device memory). Every activation stays in HBM; the
+ * entry convolution, depthwise 3x3, global pooling, residual adds and the
+ * sparse 1x1 / classifier layers (spcv_cu_spmm_layer) run as CUDA kernels, in
+ * stream order on `stream`, with a stream-ordered workspace. In
+ * SPCV_MODE_STRICT the logits are bit-identical to the reference's
+ * run_network; SPCV_MODE_FAST uses FFMA in the SpMM and cuBLAS for dense
+ * 1x1 layers. Input dims other than the model's -> SPCV_ERR_SHAPE
+ * (check_run_inputs, netdef.cpp:433-441). */
+int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images, int in_h,
+                          int in_w, int in_c, float* logits, int mode, void* stream);
 
 void spcv_cu_model_free(spcv_cu_model* m);
 

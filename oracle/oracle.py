@@ -138,6 +138,7 @@ class Ref:
         lib.ref_model_bytes.argtypes = [ctypes.c_char_p, _d, _d, ctypes.c_uint32, _p, _z,
                                         ctypes.POINTER(_z)]
         lib.ref_model_parse.argtypes = [_p, _z, ctypes.POINTER(_i)]
+        lib.ref_run_model.argtypes = [_p, _z, _p, _i, _i, _p, ctypes.POINTER(_i)]
         lib.ref_model_layer.argtypes = [_p, _z, _i, _p, _p, _p, _p, _p]
         lib.ref_bench_layers.argtypes = [ctypes.POINTER(RefLayer), _i, _i, _i, _i, ctypes.POINTER(_d)]
         lib.ref_bench_spmm.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z, _i, _i, _i, _p, _p, _i,
@@ -228,6 +229,21 @@ class Ref:
                                       ctypes.byref(n))
         assert rc == 0, rc
         return buf.tobytes()
+
+    def run_model(self, data: bytes, images_hwc: np.ndarray, reference_executor: bool = False) -> np.ndarray:
+        """run_network (or run_network_reference) per image: [B][H][W][C] -> logits [B][classes]."""
+        buf = np.frombuffer(data, dtype=np.uint8)
+        x = np.ascontiguousarray(images_hwc, dtype=np.float32)
+        classes = _i()
+        rc = self.lib.ref_run_model(buf.ctypes.data, buf.size, None, 0, 0, None, ctypes.byref(classes))
+        if rc:
+            raise RuntimeError(f"ref_run_model: code {rc}")
+        out = np.zeros((x.shape[0], classes.value), np.float32)
+        rc = self.lib.ref_run_model(buf.ctypes.data, buf.size, x.ctypes.data, x.shape[0],
+                                    1 if reference_executor else 0, out.ctypes.data, ctypes.byref(classes))
+        if rc:
+            raise RuntimeError(f"ref_run_model: code {rc}")
+        return out
 
     def model_parse(self, data: bytes):
         """parse_model: (status code, layer count)."""

@@ -360,4 +360,30 @@ int ref_model_layer(const std::uint8_t* data, std::size_t size, int i, int* meta
     }
 }
 
+// run_network (netdef.cpp:456-524; which == 0, default ExecOptions) or
+// run_network_reference (netdef.cpp:526-; which == 1) over `images` HWC images
+// [images][H][W][C] of a model file; logits [images][num_classes]. Two-call
+// on *classes (logits may be null).
+int ref_run_model(const std::uint8_t* data, std::size_t size, const float* input, int images,
+                  int which, float* logits, int* classes) {
+    try {
+        const auto parsed = spcv::parse_model(data, size);
+        const spcv::NetworkSpec& net = parsed.first;
+        if (classes) *classes = net.num_classes;
+        if (!logits) return 0;
+        const std::size_t per = static_cast<std::size_t>(net.input_h) * net.input_w * net.input_c;
+        for (int i = 0; i < images; ++i) {
+            spcv::Tensor t(net.input_c, net.input_h, net.input_w, spcv::Layout::HWC);
+            std::copy(input + i * per, input + (i + 1) * per, t.data.begin());
+            const std::vector<float> out = which == 0
+                                               ? spcv::run_network(net, parsed.second, t, spcv::ExecOptions{})
+                                               : spcv::run_network_reference(net, parsed.second, t);
+            std::copy(out.begin(), out.end(), logits + static_cast<std::size_t>(i) * out.size());
+        }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
 }  // extern "C"

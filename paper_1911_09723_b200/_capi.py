@@ -38,6 +38,7 @@ SIGNATURES = {
     "spcv_cu_model_layer": (_i, [_p, _i, _p]),
     "spcv_cu_model_weights": (_i, [_p, _i, ctypes.POINTER(_p)]),
     "spcv_cu_model_run": (_i, [_p, _i, _p, _i, _p, _p, _i, _p]),
+    "spcv_cu_model_forward": (_i, [_p, _p, _i, _i, _i, _i, _p, _i, _p]),
     "spcv_cu_model_free": (None, [_p]),
     "spcv_cu_launch_count": (_u64, []),
     "spcv_cu_last_error": (ctypes.c_char_p, []),

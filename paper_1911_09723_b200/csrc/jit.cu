@@ -155,13 +155,30 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
       << "__device__ __forceinline__ float hi32(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }\n"
       << "__device__ __forceinline__ float clampf(float v, float lo, float hi) {"
          " return v < lo ? lo : (v > hi ? hi : v); }\n";
-    // CTA -> (segment, rank in segment)
+    // CTA -> (segment, rank in segment), segments interleaved round-robin so
+    // neighbouring CTAs (and both dies) run every segment
+    std::vector<int> seg_of, rank_of, left;
+    for (const Segment& sg : segs) left.push_back(sg.ctas);
+    for (bool any = true; any;) {
+        any = false;
+        for (size_t s = 0; s < segs.size(); ++s)
+            if (left[s] > 0) {
+                seg_of.push_back(static_cast<int>(s));
+                rank_of.push_back(segs[s].ctas - left[s]);
+                --left[s];
+                any = true;
+            }
+    }
+    if (env_int("SPCV_JIT_INTERLEAVE", 1) == 0) {
+        seg_of.clear();
+        rank_of.clear();
+        for (size_t s = 0; s < segs.size(); ++s)
+            for (int c = 0; c < segs[s].ctas; ++c) seg_of.push_back(static_cast<int>(s)), rank_of.push_back(c);
+    }
     o << "__device__ const unsigned char seg_of[" << key.sms << "] = {";
-    for (size_t s = 0; s < segs.size(); ++s)
-        for (int c = 0; c < segs[s].ctas; ++c) o << s << ",";
+    for (int v : seg_of) o << v << ",";
     o << "};\n__device__ const unsigned char rank_of[" << key.sms << "] = {";
-    for (size_t s = 0; s < segs.size(); ++s)
-        for (int c = 0; c < segs[s].ctas; ++c) o << c << ",";
+    for (int v : rank_of) o << v << ",";
     o << "};\n";
 
     const int brows = M / BH;

@@ -13,9 +13,10 @@
 #include <string>
 #include <vector>
 
-#include "spcv_internal.h"
+#include "model_internal.h"
 
 using namespace spcv_detail;
+using namespace spcv_model;
 
 namespace {
 
@@ -114,37 +115,6 @@ struct Reader {
         off += static_cast<size_t>(n) * 4;
         return v;
     }
-};
-
-enum Kind : uint8_t { kEntryConv = 0, kPointwise = 1, kDepthwise = 2, kGlobalPool = 3, kFullyConnected = 4 };
-enum Storage : uint8_t { kNone = 0, kConv = 1, kDw = 2, kDense = 3, kBcsr = 4 };
-
-struct Layer {
-    uint8_t kind = 0;
-    std::string name;
-    int cin = 0, cout = 0, stride = 1, in_h = 0, in_w = 0, out_h = 0, out_w = 0;
-    bool sparse = false;
-    double sparsity = 0.0;
-    int block_h = 1;
-    int act_kind = 0;
-    float lo = 0.0f, hi = 0.0f;
-    int residual_src = -1;
-    std::vector<float> bias;
-    uint8_t storage = kNone;
-    // pointwise / classifier weights
-    int rows = 0, cols = 0, bh = 1;
-    std::vector<uint32_t> row_ptr, col_idx;
-    std::vector<float> values;  // BCSR values or dense row-major data
-    // entry conv / depthwise weights (kept on the host; not on the SpMM path)
-    std::vector<float> other;
-};
-
-struct Net {
-    std::string name;
-    int width_milli = 0, input_h = 0, input_w = 0, input_c = 0, num_classes = 0;
-    double plan_sparsity = 0.0;
-    int block_start = 0, block_h_after = 0;
-    std::vector<Layer> layers;
 };
 
 // BcsrMatrix::validate (sparse.cpp:16-51) -> message or "" when valid.
@@ -317,14 +287,6 @@ Net parse(const uint8_t* data, size_t size) {
 
 }  // namespace
 
-struct spcv_cu_model {
-    Net net;
-    int device = 0;
-    std::vector<spcv_cu_weights*> w;  // per layer: packed sparse weights (or null)
-    std::vector<float*> d_dense;      // per layer: dense row-major matrix (or null)
-    std::vector<float*> d_bias;       // per layer: bias (or null)
-};
-
 namespace {
 
 void free_model(spcv_cu_model* m) {
@@ -332,6 +294,7 @@ void free_model(spcv_cu_model* m) {
     for (auto* w : m->w) spcv_cu_free(w);
     for (float* p : m->d_dense) cudaFree(p);
     for (float* p : m->d_bias) cudaFree(p);
+    for (float* p : m->d_conv) cudaFree(p);
     delete m;
 }
 
@@ -371,8 +334,31 @@ extern "C" int spcv_cu_model_load(const uint8_t* bytes, size_t size, spcv_cu_mod
     m->w.assign(n, nullptr);
     m->d_dense.assign(n, nullptr);
     m->d_bias.assign(n, nullptr);
+    m->d_conv.assign(n, nullptr);
+    auto upload = [&](float** dst, const std::vector<float>& v, const char* what) {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(v.size(), 1) * 4);
+        if (e == cudaSuccess && !v.empty())
+            e = cudaMemcpy(*dst, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+        return e == cudaSuccess ? SPCV_OK : cuda_fail(e, what);
+    };
     for (size_t i = 0; i < n && rc == SPCV_OK; ++i) {
         const Layer& L = m->net.layers[i];
+        if (L.kind == kEntryConv) {
+            // [co][ci][ky][kx] -> [co][ky][kx][ci]: every tap reads one HWC pixel
+            // (the same repack as entry_conv_hwc_to_chw, kernels.cpp:433-441)
+            std::vector<float> wp(L.other.size());
+            for (int co = 0; co < L.cout; ++co)
+                for (int ky = 0; ky < 3; ++ky)
+                    for (int kx = 0; kx < 3; ++kx)
+                        for (int ci = 0; ci < L.cin; ++ci)
+                            wp[((static_cast<size_t>(co) * 3 + ky) * 3 + kx) * L.cin + ci] =
+                                L.other[((static_cast<size_t>(co) * L.cin + ci) * 3 + ky) * 3 + kx];
+            rc = upload(&m->d_conv[i], wp, "model: entry conv upload");
+        } else if (L.kind == kDepthwise) {
+            rc = upload(&m->d_conv[i], L.other, "model: depthwise upload");
+        }
+        if (rc == SPCV_OK && (L.kind == kEntryConv || L.kind == kDepthwise) && !L.bias.empty())
+            rc = upload(&m->d_bias[i], L.bias, "model: bias upload");
         if (L.kind != kPointwise && L.kind != kFullyConnected) continue;
         if (L.storage == kBcsr) {
             rc = spcv_cu_pack(L.rows, L.cols, L.bh, L.row_ptr.data(), L.row_ptr.size(), L.col_idx.data(),

@@ -1,0 +1,54 @@
+// model_internal.h — the parsed SPCV model (model.cu) as the device
+// executor (network.cu) sees it.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "spcv_internal.h"
+
+namespace spcv_model {
+
+enum Kind : uint8_t { kEntryConv = 0, kPointwise = 1, kDepthwise = 2, kGlobalPool = 3, kFullyConnected = 4 };
+enum Storage : uint8_t { kNone = 0, kConv = 1, kDw = 2, kDense = 3, kBcsr = 4 };
+
+struct Layer {
+    uint8_t kind = 0;
+    std::string name;
+    int cin = 0, cout = 0, stride = 1, in_h = 0, in_w = 0, out_h = 0, out_w = 0;
+    bool sparse = false;
+    double sparsity = 0.0;
+    int block_h = 1;
+    int act_kind = 0;
+    float lo = 0.0f, hi = 0.0f;
+    int residual_src = -1;
+    std::vector<float> bias;
+    uint8_t storage = kNone;
+    // pointwise / classifier weights
+    int rows = 0, cols = 0, bh = 1;
+    std::vector<uint32_t> row_ptr, col_idx;
+    std::vector<float> values;  // BCSR values or dense row-major data
+    // entry conv [co][ci][3][3] / depthwise [c][3][3] weights
+    std::vector<float> other;
+};
+
+struct Net {
+    std::string name;
+    int width_milli = 0, input_h = 0, input_w = 0, input_c = 0, num_classes = 0;
+    double plan_sparsity = 0.0;
+    int block_start = 0, block_h_after = 0;
+    std::vector<Layer> layers;
+};
+
+}  // namespace spcv_model
+
+struct spcv_cu_model {
+    spcv_model::Net net;
+    int device = 0;
+    std::vector<spcv_cu_weights*> w;  // per layer: packed sparse weights (or null)
+    std::vector<float*> d_dense;      // per layer: dense row-major matrix (or null)
+    std::vector<float*> d_bias;       // per layer: bias (or null)
+    std::vector<float*> d_conv;       // per layer: entry conv [co][ky][kx][ci] / depthwise [c][9]
+};
+

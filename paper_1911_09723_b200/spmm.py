@@ -547,6 +547,22 @@ class DeviceModel:
                                      None if residual is None else residual.data_ptr(), out.data_ptr(),
                                      _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))
 
+    def forward(self, images_hwc, strict: bool = True, stream=None):
+        """run_network on the device: torch CUDA [B][H][W][C] fp32 -> logits [B][classes]
+        (spcv_cu_model_forward; bit-exact with the reference executor in strict mode)."""
+        import torch
+
+        x = images_hwc.contiguous()
+        B, H, W, C = x.shape
+        classes = self.layers[-1]["cout"]
+        out = torch.empty((B, classes), dtype=torch.float32, device=x.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        _raise(lib.spcv_cu_model_forward(self._h, x.data_ptr(), B, H, W, C, out.data_ptr(),
+                                         _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             lib.spcv_cu_model_free(self._h)

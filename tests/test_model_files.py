@@ -108,3 +108,39 @@ def test_device_model_matches_reference_layers(ref, oracle, files, name):
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), L
         checked += 1
     assert checked > 5
+
+
+# ----------------------------------------- the whole executor on the device
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [f"{a}-{w}" for a, w, _ in MODELS])
+def test_device_forward_bit_exact_with_run_network(ref, files, name):
+    """spcv_cu_model_forward (entry conv, depthwise, pooling, residuals and the
+    sparse / dense 1x1 layers, all on the device) returns the reference
+    run_network's logits bit for bit in strict mode; fast mode stays close."""
+    import torch
+
+    data = files[name]
+    m = sp.DeviceModel(data)
+    L0 = m.layers[0]
+    B = 3
+    x = np.random.default_rng(11).uniform(-1, 1, (B, L0["in_h"], L0["in_w"], L0["cin"])).astype(np.float32)
+    want = ref.run_model(data, x)
+    got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert got.shape == want.shape
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), float(np.abs(got - want).max())
+    fast = m.forward(torch.from_numpy(x).cuda(), strict=False).cpu().numpy()
+    assert np.allclose(fast, want, rtol=1e-3, atol=1e-3 * float(np.abs(want).max()))
+    # images are independent: a batch of one reproduces its row
+    one = m.forward(torch.from_numpy(x[1:2]).cuda()).cpu().numpy()
+    assert np.array_equal(one.view(np.uint32), want[1:2].view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_device_forward_checks_input_shape(files):
+    import torch
+
+    m = sp.DeviceModel(files["mbv1-0.25"])
+    L0 = m.layers[0]
+    with pytest.raises(sp.ShapeError):
+        m.forward(torch.zeros(1, L0["in_h"] + 1, L0["in_w"], L0["cin"], device="cuda"))
+    assert m.forward(torch.zeros(0, L0["in_h"], L0["in_w"], L0["cin"], device="cuda")).shape[0] == 0
