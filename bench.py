@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the cuBLAS dense fp32 baseline")
     ap.add_argument("--cpu-images", type=int, default=None, help="CPU baseline sample, images")
     ap.add_argument("--layers-json", default=None, help="write per-layer results here")
+    ap.add_argument("--no-network", action="store_true",
+                    help="skip the whole-network (device executor) measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")
@@ -264,7 +266,9 @@ def main():
                               bh=d.layer.block_h, nnz=d.nnz, row_slots=mode_cfg[d.layer.name],
                               us=us, gflops=d.flops() / us / 1e3, gbs=d.alg_bytes() / us / 1e3,
                               hbm_frac=d.alg_bytes() / us / 1e3 / hbm_peak,
-                              alg_bytes=d.alg_bytes(), flops=d.flops()))
+                              alg_bytes=d.alg_bytes(), flops=d.flops(),
+                              kernel=("spcv_jit" if dev_layers[li][0].kernel(args.mode == "strict") == "jit"
+                                      else "spmm_bcsr_kernel")))
     tot_us = sum(p["us"] for p in per_layer)
     for p in per_layer:
         p["share"] = p["us"] / tot_us
@@ -375,6 +379,12 @@ def main():
             if not np.array_equal(o_dev.cpu().numpy().view(np.uint32), o.view(np.uint32)):
                 raise SystemExit("e2e output differs from the device-path output")
 
+    # ---- the whole network on the device (run_network: entry conv, depthwise,
+    # pooling, sparse 1x1 layers, classifier), informational beside the headline
+    network = None
+    if not args.no_network:
+        network = bench_network(args, dev, stream, dist, images)
+
     # ---- CPU baseline (rank 0, N=1 only), a bounded sample of the same workload
     cpu = None
     if dist.world == 1 and not args.no_cpu:
@@ -398,7 +408,7 @@ def main():
     if dist.rank == 0:
         roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(dom["gbs"] / hbm_peak, 4), "traffic": traffic,
-                    "kernel": f"spmm_bcsr_kernel [{dom['name']}: {dom['K']}->{dom['M']} @S={dom['S']}]",
+                    "kernel": f"{dom.get('kernel', 'tile')} [{dom['name']}: {dom['K']}->{dom['M']} @S={dom['S']}]",
                     "peak_kind": peak_kind,
                     "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": round(dom["us"], 2),
                     "share_of_step": round(dom["share"], 3),
@@ -424,6 +434,7 @@ def main():
                              f"per GPU vs 126 MB L2, no explicit flush"},
             "hbm_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "dense_baseline": dense,
+            "network": network,
             "gpu_launches": launches, "clocks": clk.summary(),
             "modes": {args.mode: {"value": round(value, 3), "ms_per_step": round(ms_step, 4)},
                       other: {"value": round(flops_all / (ms_alt * 1e-3) / 1e9, 3),
@@ -433,6 +444,73 @@ def main():
         }
         print(json.dumps(line), flush=True)
     dist.close()
+
+
+def bench_network(args, dev, stream, dist, batch):
+    """MobileNet-v1-1.0 @224 as an SPCV model file (netfile.py: the reference's
+    builder / default_plan / serializer restated, seeded synthetic weights),
+    run end to end by spcv_cu_model_forward on `batch` images per GPU. Sparse
+    strict and fast, the densified network (dense 1x1 via cuBLAS, fast), and
+    batch-1 latency; CUDA events on the launch stream, max over ranks."""
+    import torch
+
+    import paper_1911_09723_b200 as sp
+    from paper_1911_09723_b200 import netfile
+
+    net = netfile.build_mbv1(1.0, 0.9, seed=11)
+    blob = netfile.serialize(net)
+    m = sp.DeviceModel(blob)
+    md = sp.DeviceModel(netfile.serialize(netfile.densify(net)))
+    rng = np.random.default_rng(100 + dist.rank)
+    x = torch.from_numpy(rng.uniform(-1, 1, (batch, 224, 224, 3)).astype(np.float32)).to(dev)
+
+    def timed(model, strict, inp, steps):
+        with torch.cuda.stream(stream):
+            for _ in range(max(2, args.warmup)):
+                model.forward(inp, strict, stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier(dev)
+            torch.cuda.synchronize()
+            n0 = sp.launch_count()
+            e0.record(stream)
+            for _ in range(steps):
+                model.forward(inp, strict, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            launches = (sp.launch_count() - n0) // steps
+        return dist.max(e0.elapsed_time(e1), device=torch.device("cuda", dev)) / steps, launches
+
+    steps = max(3, min(args.steps, 10))
+    ms_strict, launches = timed(m, True, x, steps)
+    ms_fast, _ = timed(m, False, x, steps)
+    ms_dense, _ = timed(md, False, x, steps)
+    ms_b1, _ = timed(m, True, x[:1], 20)
+    log(f"network MBv1-1.0 x{batch}: strict {ms_strict:.3f} ms, fast {ms_fast:.3f} ms, "
+        f"dense(cuBLAS) {ms_dense:.3f} ms, batch-1 latency {ms_b1:.3f} ms")
+    out = {"model": "MobileNet-v1-1.0 @224x224x3: entry conv, 13 depthwise + 13 sparse 1x1 (90%, "
+                    "4x1 blocks from pw12: the reference's default_plan), pool, dense classifier",
+           "images_per_gpu": batch, "mode": "strict",
+           "images_per_s": round(batch * dist.world / (ms_strict * 1e-3), 1),
+           "ms_per_batch": round(ms_strict, 3), "fast_ms_per_batch": round(ms_fast, 3),
+           "dense_cublas_ms_per_batch": round(ms_dense, 3),
+           "sparse_speedup_vs_dense": round(ms_dense / ms_fast, 2),
+           "batch1_latency_ms": round(ms_b1, 3), "gpu_launches_per_forward": launches,
+           "how": "spcv_cu_model_forward: every activation device-resident; strict = bit-exact "
+                  "with the reference run_network (tests/test_model_files.py)"}
+    if dist.world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as orc  # CPU baseline leg: the reference executor itself
+
+        ref = orc.Ref()
+        xs = x[:2].cpu().numpy()
+        ref.run_model(blob, xs[:1])
+        t0 = time.perf_counter()
+        ref.run_model(blob, xs)
+        dt = (time.perf_counter() - t0) / xs.shape[0]
+        out["reference_cpu"] = {"images_per_s": round(1.0 / dt, 2), "cores": 1, "kind": "reference",
+                                "sample": "run_network (oracle/_ref, default ExecOptions) on 2 images, "
+                                          "one thread (the reference executor is single-threaded)"}
+    return out
 
 
 def run_reference(args, layers, images):

@@ -42,6 +42,24 @@ __device__ __forceinline__ float act_apply(float v, int kind, float lo, float hi
     return kind == 1 ? (v < lo ? lo : (v > hi ? hi : v)) : v;
 }
 
+// Division by a runtime constant for n < 2^31 (round-up multiplier, as in
+// CUTLASS's FastDivmod): q = umulhi(n, m) >> (p - 32), p = 31 + ceil(log2 d).
+struct FastDiv {
+    uint32_t d = 1, m = 0, shift = 0;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t div) : d(div) {
+        if (d <= 1) return;
+        uint32_t l = 0;
+        while ((1ull << l) < d) ++l;
+        const uint32_t p = 31 + l;
+        m = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
+        shift = p - 32;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return d == 1 ? n : (__umulhi(n, m) >> shift);
+    }
+};
+
 struct ConvArgs {
     const float* in;
     const float* w;
@@ -53,54 +71,196 @@ struct ConvArgs {
 };
 
 // Entry convolution: HWC image -> CHW, 3x3 taps, weights [co][ky][kx][ci].
+// One thread per output pixel (image, oy, ox): its 9*C input taps are loaded
+// once into registers (C <= kMaxEntryC), then every output channel is summed
+// from them with the weights read from shared memory (warp-uniform, broadcast).
+// Taps outside the image are skipped, as in the reference (not added as 0).
+constexpr int kMaxEntryC = 4;
 __global__ void entry_conv_kernel(const ConvArgs a) {
-    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (i >= a.total) return;
-    const int ox = static_cast<int>(i % a.OW);
-    const int oy = static_cast<int>((i / a.OW) % a.OH);
-    const int co = static_cast<int>((i / (static_cast<long long>(a.OW) * a.OH)) % a.CO);
-    const long long img = i / (static_cast<long long>(a.OW) * a.OH * a.CO);
+    extern __shared__ float wsm[];  // [CO][9*C] + bias[CO]
+    const int taps = 9 * a.C;
+    for (int i = threadIdx.x; i < a.CO * taps; i += blockDim.x) wsm[i] = a.w[i];
+    float* bsm = wsm + a.CO * taps;
+    for (int i = threadIdx.x; i < a.CO; i += blockDim.x) bsm[i] = a.bias ? a.bias[i] : 0.0f;
+    __syncthreads();
+    const long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long npix = a.total / a.CO;  // images * OH * OW
+    if (pix >= npix) return;
+    const int plane = a.OH * a.OW;
+    const long long img = pix / plane;
+    const int p = static_cast<int>(pix - img * plane);
+    const int oy = p / a.OW, ox = p - oy * a.OW;
     const float* src = a.in + img * a.H * a.W * a.C;
-    const float* kb = a.w + static_cast<long long>(co) * 9 * a.C;
-    float acc = a.bias ? a.bias[co] : 0.0f;
+    float x[9 * kMaxEntryC];
+    bool ok[9];
     const int iy0 = oy * a.stride - a.pad_t, ix0 = ox * a.stride - a.pad_l;
-    for (int ky = 0; ky < 3; ++ky) {
-        const int iy = iy0 + ky;
-        if (static_cast<unsigned>(iy) >= static_cast<unsigned>(a.H)) continue;
-        for (int kx = 0; kx < 3; ++kx) {
-            const int ix = ix0 + kx;
-            if (static_cast<unsigned>(ix) >= static_cast<unsigned>(a.W)) continue;
-            const float* px = src + (static_cast<long long>(iy) * a.W + ix) * a.C;
-            const float* kk = kb + (ky * 3 + kx) * a.C;
-            for (int ci = 0; ci < a.C; ++ci) acc = __fadd_rn(acc, __fmul_rn(kk[ci], px[ci]));
-        }
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int iy = iy0 + t / 3, ix = ix0 + t % 3;
+        ok[t] = static_cast<unsigned>(iy) < static_cast<unsigned>(a.H) &&
+                static_cast<unsigned>(ix) < static_cast<unsigned>(a.W);
+        const float* px = src + (static_cast<long long>(ok[t] ? iy : 0) * a.W + (ok[t] ? ix : 0)) * a.C;
+#pragma unroll
+        for (int ci = 0; ci < kMaxEntryC; ++ci) x[t * kMaxEntryC + ci] = ci < a.C ? px[ci] : 0.0f;
     }
-    a.out[i] = act_apply(acc, a.act_kind, a.lo, a.hi);
+    float* dst = a.out + img * a.CO * plane + p;
+    for (int co = 0; co < a.CO; ++co) {
+        const float* k = wsm + co * taps;
+        float acc = bsm[co];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            if (!ok[t]) continue;
+#pragma unroll
+            for (int ci = 0; ci < kMaxEntryC; ++ci)
+                if (ci < a.C) acc = __fadd_rn(acc, __fmul_rn(k[t * a.C + ci], x[t * kMaxEntryC + ci]));
+        }
+        dst[static_cast<long long>(co) * plane] = act_apply(acc, a.act_kind, a.lo, a.hi);
+    }
 }
 
-// Depthwise 3x3, CHW in and out, weights [c][ky][kx].
-__global__ void depthwise_kernel(const ConvArgs a) {
-    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (i >= a.total) return;
-    const int ox = static_cast<int>(i % a.OW);
-    const int oy = static_cast<int>((i / a.OW) % a.OH);
-    const long long plane = i / (static_cast<long long>(a.OW) * a.OH);  // img * C + c
-    const int c = static_cast<int>(plane % a.CO);
-    const float* src = a.in + plane * a.H * a.W;
-    const float* k = a.w + c * 9;
-    float acc = a.bias ? a.bias[c] : 0.0f;
+// Entry convolution with the weights in the kernel's parameter space (a
+// __grid_constant__ struct, <= 32 KB): every FMUL takes its weight straight
+// from the constant bank at a compile-time offset, no load instruction.
+// Instantiated for C = 3 and the entry widths round_channels(32|16, width)
+// produces (multiples of 8 up to 64).
+template <int C, int CO>
+struct EntryParams {
+    float w[CO * 9 * C];  // [co][ky][kx][ci]
+    float b[CO];
+};
+
+template <int C, int CO>
+__global__ void __launch_bounds__(128) entry_conv_const(const ConvArgs a, const __grid_constant__ EntryParams<C, CO> prm) {
+    const long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long npix = a.total / CO;
+    if (pix >= npix) return;
+    const int plane = a.OH * a.OW;
+    const long long img = pix / plane;
+    const int p = static_cast<int>(pix - img * plane);
+    const int oy = p / a.OW, ox = p - oy * a.OW;
+    const float* src = a.in + img * a.H * a.W * C;
+    float x[9 * C];
+    bool ok[9];
     const int iy0 = oy * a.stride - a.pad_t, ix0 = ox * a.stride - a.pad_l;
-    for (int ky = 0; ky < 3; ++ky) {
-        const int iy = iy0 + ky;
-        if (static_cast<unsigned>(iy) >= static_cast<unsigned>(a.H)) continue;
-        const float* row = src + static_cast<long long>(iy) * a.W;
-        for (int kx = 0; kx < 3; ++kx) {
-            const int ix = ix0 + kx;
-            if (static_cast<unsigned>(ix) >= static_cast<unsigned>(a.W)) continue;
-            acc = __fadd_rn(acc, __fmul_rn(k[ky * 3 + kx], row[ix]));
-        }
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int iy = iy0 + t / 3, ix = ix0 + t % 3;
+        ok[t] = static_cast<unsigned>(iy) < static_cast<unsigned>(a.H) &&
+                static_cast<unsigned>(ix) < static_cast<unsigned>(a.W);
+        const float* px = src + (static_cast<long long>(ok[t] ? iy : 0) * a.W + (ok[t] ? ix : 0)) * C;
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) x[t * C + ci] = __ldg(px + ci);
     }
-    a.out[i] = act_apply(acc, a.act_kind, a.lo, a.hi);
+    float* dst = a.out + img * CO * plane + p;
+    bool interior = true;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) interior = interior && ok[t];
+    if (interior) {  // no tap skipped: straight-line code
+#pragma unroll
+        for (int co = 0; co < CO; ++co) {
+            float acc = a.bias ? prm.b[co] : 0.0f;
+#pragma unroll
+            for (int t = 0; t < 9 * C; ++t) acc = __fadd_rn(acc, __fmul_rn(prm.w[co * 9 * C + t], x[t]));
+            __stcs(dst + static_cast<long long>(co) * plane, act_apply(acc, a.act_kind, a.lo, a.hi));
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int co = 0; co < CO; ++co) {
+        float acc = a.bias ? prm.b[co] : 0.0f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            if (!ok[t]) continue;
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci)
+                acc = __fadd_rn(acc, __fmul_rn(prm.w[(co * 9 + t) * C + ci], x[t * C + ci]));
+        }
+        __stcs(dst + static_cast<long long>(co) * plane, act_apply(acc, a.act_kind, a.lo, a.hi));
+    }
+}
+
+template <int CO>
+bool launch_entry_const(const ConvArgs& a, const std::vector<float>& w_cikk, const std::vector<float>& bias,
+                        unsigned grid, cudaStream_t st) {
+    EntryParams<3, CO> prm;
+    for (int co = 0; co < CO; ++co)
+        for (int t = 0; t < 9; ++t)
+            for (int ci = 0; ci < 3; ++ci)  // [co][ci][ky][kx] -> [co][ky][kx][ci]
+                prm.w[(co * 9 + t) * 3 + ci] = w_cikk[(static_cast<size_t>(co) * 3 + ci) * 9 + t];
+    for (int co = 0; co < CO; ++co) prm.b[co] = bias.empty() ? 0.0f : bias[static_cast<size_t>(co)];
+    entry_conv_const<3, CO><<<grid, 128, 0, st>>>(a, prm);
+    return true;
+}
+
+bool launch_entry_fast(const ConvArgs& a, int C, int CO, const std::vector<float>& w,
+                       const std::vector<float>& bias, unsigned grid, cudaStream_t st) {
+    if (C != 3) return false;
+    switch (CO) {
+        case 8: return launch_entry_const<8>(a, w, bias, grid, st);
+        case 16: return launch_entry_const<16>(a, w, bias, grid, st);
+        case 24: return launch_entry_const<24>(a, w, bias, grid, st);
+        case 32: return launch_entry_const<32>(a, w, bias, grid, st);
+        case 40: return launch_entry_const<40>(a, w, bias, grid, st);
+        case 48: return launch_entry_const<48>(a, w, bias, grid, st);
+        case 56: return launch_entry_const<56>(a, w, bias, grid, st);
+        case 64: return launch_entry_const<64>(a, w, bias, grid, st);
+        default: return false;
+    }
+}
+
+// Depthwise 3x3, CHW in and out, weights [c][ky][kx]. A thread computes the
+// outputs (oy .. oy+3, ox) of one column strip: it loads the 3 x (3*STRIDE+?)
+// input window rows once into registers (consecutive lanes = consecutive ox:
+// coalesced row loads), then sums each output's taps in the reference order.
+template <int STRIDE>
+__global__ void depthwise_kernel(const ConvArgs a, uint32_t items, int RB, FastDiv div_ow, FastDiv div_rb,
+                                 FastDiv div_c) {
+    constexpr int kRows = 4;                      // outputs per thread (vertical)
+    constexpr int kIn = (kRows - 1) * STRIDE + 3;  // input rows in the window
+    const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= items) return;
+    const uint32_t strip = div_ow.div(it);        // plane * RB + rb
+    const int ox = static_cast<int>(it - strip * a.OW);
+    const uint32_t plane = div_rb.div(strip);
+    const int oy0 = static_cast<int>(strip - plane * RB) * kRows;
+    const int c = static_cast<int>(plane - div_c.div(plane) * a.CO);
+    const float* src = a.in + static_cast<long long>(plane) * a.H * a.W;
+    float k[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) k[t] = __ldg(a.w + c * 9 + t);
+    const float b = a.bias ? __ldg(a.bias + c) : 0.0f;
+    const int ix0 = ox * STRIDE - a.pad_l, iy0 = oy0 * STRIDE - a.pad_t;
+    bool cok[3];
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) cok[kx] = static_cast<unsigned>(ix0 + kx) < static_cast<unsigned>(a.W);
+    float v[kIn][3];
+    bool rok[kIn];
+#pragma unroll
+    for (int r = 0; r < kIn; ++r) {
+        const int iy = iy0 + r;
+        rok[r] = static_cast<unsigned>(iy) < static_cast<unsigned>(a.H);
+        const float* row = src + static_cast<long long>(rok[r] ? iy : 0) * a.W;
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) v[r][kx] = (rok[r] && cok[kx]) ? __ldg(row + ix0 + kx) : 0.0f;
+    }
+    float* dst = a.out + static_cast<long long>(plane) * a.OH * a.OW + ox;
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+        const int oy = oy0 + j;
+        if (oy >= a.OH) break;
+        float acc = b;
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+            const int r = j * STRIDE + ky;
+            if (!rok[r]) continue;
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+                if (!cok[kx]) continue;  // tap outside the image: skipped (kernels.cpp:414-416)
+                acc = __fadd_rn(acc, __fmul_rn(k[ky * 3 + kx], v[r][kx]));
+            }
+        }
+        dst[static_cast<long long>(oy) * a.OW] = act_apply(acc, a.act_kind, a.lo, a.hi);
+    }
 }
 
 // Global average pool: one thread per (image, channel), sequential sum.
@@ -232,10 +392,38 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
                 const Pad ph = same_pad(L.in_h, 3, L.stride), pw = same_pad(L.in_w, 3, L.stride);
                 ConvArgs a{cur, m->d_conv[i], m->d_bias[i], dst, out_elems, L.in_h, L.in_w, L.cin, L.cout,
                            ph.out, pw.out, L.stride, ph.before, pw.before, L.act_kind, L.lo, L.hi};
-                if (L.kind == kEntryConv)
-                    entry_conv_kernel<<<blocks_for(out_elems, kT), kT, 0, st>>>(a);
-                else
-                    depthwise_kernel<<<blocks_for(out_elems, kT), kT, 0, st>>>(a);
+                if (L.kind == kEntryConv) {
+                    if (L.cin > kMaxEntryC) {
+                        rc = fail(SPCV_ERR_UNSUPPORTED, "model: entry convolution with more than 4 input channels");
+                        break;
+                    }
+                    const long long npix = static_cast<long long>(images) * ph.out * pw.out;
+                    if (!launch_entry_fast(a, L.cin, L.cout, L.other, L.bias, blocks_for(npix, 128), st)) {
+                        const size_t smem = (static_cast<size_t>(L.cout) * 9 * L.cin + L.cout) * sizeof(float);
+                        entry_conv_kernel<<<blocks_for(npix, 128), 128, smem, st>>>(a);
+                    }
+                } else {
+                    if (L.stride != 1 && L.stride != 2) {
+                        rc = fail(SPCV_ERR_SHAPE, "depthwise_conv_chw: stride must be 1 or 2");
+                        break;
+                    }
+                    // 4-row strips per plane; launched in image chunks of < 2^31 threads
+                    const int RB = (ph.out + 3) / 4;
+                    const long long per_img = static_cast<long long>(L.cout) * RB * pw.out;
+                    const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
+                    const FastDiv dow(pw.out), drb(RB), dc(L.cout);
+                    for (int i0 = 0; i0 < images; i0 += chunk) {
+                        const int ni = std::min(chunk, images - i0);
+                        ConvArgs c = a;
+                        c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
+                        c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
+                        const uint32_t items = static_cast<uint32_t>(per_img * ni);
+                        if (L.stride == 1)
+                            depthwise_kernel<1><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
+                        else
+                            depthwise_kernel<2><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
+                    }
+                }
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 break;
             }
