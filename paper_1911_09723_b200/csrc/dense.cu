@@ -90,11 +90,17 @@ extern "C" int spcv_cu_dense_gemm_into(const float* w, int rows, int cols, const
     // Row-major out[b] (M x S) = W (M x K) * act[b] (K x S)  <=>  column-major
     // out[b]^T (S x M) = act[b]^T (S x K) * W^T (K x M).
     const float one = 1.0f, zero = 0.0f;
-    const cublasStatus_t cs = cublasSgemmStridedBatched(
-        h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(S), rows, cols, &one, act, static_cast<int>(S),
-        static_cast<long long>(cols) * S, w, cols, 0, &zero, out, static_cast<int>(S),
-        static_cast<long long>(rows) * S, images);
-    if (cs != CUBLAS_STATUS_SUCCESS) return fail(SPCV_ERR_CUDA, "dense_gemm: cublasSgemmStridedBatched failed");
+    // S == 1 (the classifier): the images are the GEMM's columns, one SGEMM
+    // instead of `images` matrix-vector products: column-major out (M x B) =
+    // W^T' (W row-major = K x M column-major, transposed) * act (K x B).
+    const cublasStatus_t cs =
+        S == 1 ? cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, rows, images, cols, &one, w, cols, act, cols,
+                             &zero, out, rows)
+               : cublasSgemmStridedBatched(
+                     h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(S), rows, cols, &one, act,
+                     static_cast<int>(S), static_cast<long long>(cols) * S, w, cols, 0, &zero, out,
+                     static_cast<int>(S), static_cast<long long>(rows) * S, images);
+    if (cs != CUBLAS_STATUS_SUCCESS) return fail(SPCV_ERR_CUDA, "dense_gemm: cuBLAS SGEMM failed");
     const long long total = static_cast<long long>(images) * rows * S;
     if (bias_len || act_kind != SPCV_ACT_NONE) {
         const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 32));

@@ -560,8 +560,9 @@ def test_jit_odd_spatial_falls_back_to_tile_bit_exact(oracle):
 
 # ------------------------------------------------- dense fp32 baseline (§8f-1)
 @pytest.mark.parametrize("layer", [mbv1_pointwise()[0], mbv1_pointwise()[6], mbv1_pointwise()[12],
-                                   Layer("odd", 40, 24, 5, 7, sparsity=0.0)],
-                         ids=["pw1", "pw7", "pw13", "odd"])
+                                   Layer("odd", 40, 24, 5, 7, sparsity=0.0),
+                                   Layer("fc", 1024, 1000, 1, 1, ("none", 0.0, 0.0), -1.0, 1.0, 0.0)],
+                         ids=["pw1", "pw7", "pw13", "odd", "classifier_s1"])
 def test_dense_baseline_within_fp32_rounding(oracle, layer):
     """dense_gemm_into (kernels.cpp:345-373) through cuBLAS SGEMM (pedantic
     fp32): within the fp32 reordering bound of the dense oracle (the reference's

@@ -19,7 +19,27 @@ MODELS = [("mbv1", 0.25, 0.9), ("mbv2", 0.35, 0.8), ("ca-mbv2", 1.0, 0.85)]
 
 @pytest.fixture(scope="module")
 def files(ref):
-    return {f"{a}-{w}": ref.model_bytes(a, w, s, 7) for a, w, s in MODELS}
+    from paper_1911_09723_b200 import netfile
+
+    out = {f"{a}-{w}": ref.model_bytes(a, w, s, 7) for a, w, s in MODELS}
+    net = netfile.build_mbv1(0.25, 0.9, seed=3)
+    out["ours-mbv1-0.25"] = netfile.serialize(net)          # python-written file
+    out["ours-mbv1-0.25-dense"] = netfile.serialize(netfile.densify(net))
+    return out
+
+
+def test_python_written_files_parse_like_reference_files(ref, files):
+    """netfile.py (the MBv1 builder + serialize_model restated) writes files the
+    reference's parse_model accepts, with the layer list of build_mbv1."""
+    for name in ("ours-mbv1-0.25", "ours-mbv1-0.25-dense"):
+        rc, n = ref.model_parse(files[name])
+        assert rc == 0 and n == 29, name
+        assert sp.parse_model_status(files[name]) == 0
+        ref_meta = [ref.model_layer(files["mbv1-0.25"], i)[0] for i in range(29)]
+        our_meta = [ref.model_layer(files[name], i)[0] for i in range(29)]
+        for a, b in zip(ref_meta, our_meta):
+            assert (a["kind"], a["cin"], a["cout"], a["residual_src"]) == (b["kind"], b["cin"], b["cout"],
+                                                                           b["residual_src"])
 
 
 def test_reference_files_parse(ref, files):
@@ -112,7 +132,7 @@ def test_device_model_matches_reference_layers(ref, oracle, files, name):
 
 # ----------------------------------------- the whole executor on the device
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", [f"{a}-{w}" for a, w, _ in MODELS])
+@pytest.mark.parametrize("name", [f"{a}-{w}" for a, w, _ in MODELS] + ["ours-mbv1-0.25", "ours-mbv1-0.25-dense"])
 def test_device_forward_bit_exact_with_run_network(ref, files, name):
     """spcv_cu_model_forward (entry conv, depthwise, pooling, residuals and the
     sparse / dense 1x1 layers, all on the device) returns the reference
