@@ -533,6 +533,15 @@ thread_local HostScratch g_scratch;
 
 constexpr size_t kHostChunkBytes = 48u << 20;  // activations + outputs per pipelined chunk
 
+size_t host_chunk_bytes() {
+    static const size_t b = [] {
+        const char* e = std::getenv("SPCV_HOST_CHUNK_MB");
+        const long v = e ? std::atol(e) : 0;
+        return v > 0 ? static_cast<size_t>(v) << 20 : kHostChunkBytes;
+    }();
+    return b;
+}
+
 }  // namespace
 
 extern "C" int spcv_cu_spmm_into(const spcv_cu_weights* w, const float* act, int act_layout,
@@ -615,7 +624,7 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
 
     // Image chunks of ~kHostChunkBytes; each chunk: H2D -> kernel -> D2H.
     const size_t per_image = S * (static_cast<size_t>(act_c) + out_c) * sizeof(float);
-    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(images, kHostChunkBytes / std::max<size_t>(per_image, 1))));
+    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(images, host_chunk_bytes() / std::max<size_t>(per_image, 1))));
     const int nchunks = images > 0 ? (images + chunk - 1) / chunk : 0;
     while (static_cast<int>(hs.ev_in.size()) < nchunks) {
         cudaEvent_t a = nullptr, b = nullptr;
