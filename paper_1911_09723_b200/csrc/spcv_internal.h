@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <deque>
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -57,7 +58,7 @@ struct spcv_cu_weights {
     bool jit_eligible = false;
     std::vector<uint32_t> h_row_ptr, h_col_idx;
     std::vector<float> h_values;
-    std::vector<JitVariant> jit;
+    std::deque<JitVariant> jit;  // deque: variants never move (launching threads hold pointers)
 };
 
 namespace spcv_detail {

@@ -654,3 +654,46 @@ def test_spmm_layer_checks():
     with pytest.raises(sp.ShapeError):
         sp.spmm_layer(dw, torch.zeros(1, 9, 2, 2, device="cuda"), None, NONE,
                       torch.zeros(1, 10, 2, 2, device="cuda"))
+
+
+def test_jit_variants_compile_concurrently(oracle):
+    """Several host threads hit one packed matrix with different call shapes
+    (strict/fast x bias/no bias x clamp/none) at once: every variant compiles
+    once under the weights' lock, launches stay valid, strict results exact."""
+    import threading
+
+    import torch
+
+    layer = Layer("cc", 48, 64, 8, 8, sparsity=0.8)
+    d = make_layer_data(layer, 3, 21)
+    dw = sp.DeviceBcsr(d.weights)
+    a = torch.from_numpy(d.act).cuda()
+    b = torch.from_numpy(d.bias).cuda()
+    shapes = [(strict, bias, fused) for strict in (True, False) for bias in (True, False)
+              for fused in (RELU6, NONE)]
+    want = {(True, bias, fused.kind): oracle.spmm(d.weights, d.act, d.bias if bias else None, fused)
+            for _, bias, fused in shapes}
+    errors = []
+
+    def work(tid):
+        try:
+            st = torch.cuda.Stream()
+            for it in range(6):
+                strict, bias, fused = shapes[(tid + it) % len(shapes)]
+                o = torch.empty(3, 64, 8, 8, device="cuda")
+                sp.spmm_batched_into(dw, a, b if bias else None, fused, o,
+                                     sp.MicrokernelConfig(n=1, strict=strict), stream=st)
+                st.synchronize()
+                if strict:
+                    ref = want[(True, bias, fused.kind)].reshape(o.shape)
+                    if not np.array_equal(bits(o.cpu().numpy()), bits(ref)):
+                        errors.append((tid, it))
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
