@@ -226,14 +226,47 @@ def main():
         with ClockProbe(dev) as clk:
             start.record(stream)
             for k in range(args.steps):
-                step(lev[k])
+                step()
             end.record(stream)
             torch.cuda.synchronize()
         launches = sp.launch_count() - launches0
         dist.barrier(dev)
+        # per-layer breakdown: a separate pass with events around every launch
+        # (kept out of the headline region: the event records add gaps)
+        for k in range(args.steps):
+            step(lev[k])
+        torch.cuda.synchronize()
     ms_local = start.elapsed_time(end)
     ms_total = dist.max(ms_local, device=torch.device("cuda", dev))
     ms_step = ms_total / args.steps
+
+    # The same step replayed as one CUDA graph (the 13 launches captured once):
+    # launch overhead out of the way, which matters for the batch-1 configs.
+    graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            step()  # every kernel variant exists before capture
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                step()
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.barrier(dev)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms_graph = dist.max(e0.elapsed_time(e1), device=torch.device("cuda", dev)) / args.steps
+        graph = {"ms_per_step": round(ms_graph, 4),
+                 "value": round(dist.sum(flops_step, device=torch.device("cuda", dev)) / (ms_graph * 1e-3) / 1e9, 3),
+                 "how": "torch.cuda.CUDAGraph capture of one step (13 spcv_cu_spmm_into launches), replayed"}
+        del g
+    except Exception as e:  # noqa: BLE001 - reported, the eager number stands
+        graph = {"unavailable": repr(e)[:200]}
 
     # The other arithmetic mode on the same packed weights (reported beside the
     # headline, which is the mode selected by --mode): strict = bit-exact,
@@ -394,8 +427,21 @@ def main():
         if n_img < images:
             sample = [make_layer_data(d.layer, n_img, 1000 * (li + 1)) for li, d in enumerate(data)]
         kind, flops, times = cpu_reference_run(sample, 3, 1, threads)
+        # the reference's own concurrency model (one thread), on an 8-image slice
+        s1 = [make_layer_data(d.layer, min(8, images), 1000 * (li + 1)) for li, d in enumerate(data)]
+        _, flops1, times1 = cpu_reference_run(s1, 3, 1, 1)
+        cpu_model = ""
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    cpu_model = line.split(":", 1)[1].strip()
+                    break
+        except OSError:
+            pass
         cpu = {"value": round(flops / statistics.median(times) / 1e9, 3), "unit": "GFLOP/s",
-               "cores": threads, "kind": kind,
+               "cores": threads, "kind": kind, "cpu_model": cpu_model,
+               "single_thread": {"value": round(flops1 / statistics.median(times1) / 1e9, 3),
+                                 "sample": f"{min(8, images)} images x all layers, 1 thread, median of 3"},
                "sample": f"{n_img} image(s) x all {len(layers)} layers of {args.config} "
                          f"(= {'the full step' if n_img == images else 'a slice of the step'}), "
                          f"(layer,image) spmm_into units over {threads} threads, median of 3 passes "
@@ -434,7 +480,7 @@ def main():
                              f"per GPU vs 126 MB L2, no explicit flush"},
             "hbm_gbs": round(bytes_step / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "dense_baseline": dense,
-            "network": network,
+            "network": network, "graph": graph,
             "gpu_launches": launches, "clocks": clk.summary(),
             "modes": {args.mode: {"value": round(value, 3), "ms_per_step": round(ms_step, 4)},
                       other: {"value": round(flops_all / (ms_alt * 1e-3) / 1e9, 3),
