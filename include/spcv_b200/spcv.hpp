@@ -191,6 +191,71 @@ void spmm_batched_into(const DeviceBcsr& w, const float* d_act, int images, int 
                        const float* d_bias, const Activation& fused, float* d_out,
                        const MicrokernelConfig& cfg = {}, void* stream = nullptr);
 
+// ------------------------------------------------------------ model files
+/// model_io.hpp:13-41: the model-file error family.
+class ModelIoError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class BadMagicError : public ModelIoError {
+public:
+    using ModelIoError::ModelIoError;
+};
+class UnsupportedVersionError : public ModelIoError {
+public:
+    using ModelIoError::ModelIoError;
+};
+class TruncatedError : public ModelIoError {
+public:
+    using ModelIoError::ModelIoError;
+};
+class ChecksumError : public ModelIoError {
+public:
+    using ModelIoError::ModelIoError;
+};
+class ModelFormatError : public ModelIoError {
+public:
+    using ModelIoError::ModelIoError;
+};
+
+/// An SPCV model file (parse_model, model_io.cpp:238-381: same checks, same
+/// typed errors) uploaded once onto the current CUDA device, and the executor
+/// (run_network, netdef.cpp:456-524) over it with every activation on the device.
+class DeviceModel {
+public:
+    explicit DeviceModel(std::span<const std::uint8_t> bytes);
+    /// load_model (model_io.cpp): read the file, then as above.
+    static DeviceModel load(const std::string& path);
+    DeviceModel(const DeviceModel&) = delete;
+    DeviceModel& operator=(const DeviceModel&) = delete;
+    DeviceModel(DeviceModel&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {
+        for (int i = 0; i < 5; ++i) meta_[i] = o.meta_[i];
+    }
+    ~DeviceModel();
+
+    int num_layers() const { return meta_[0]; }
+    int input_h() const { return meta_[1]; }
+    int input_w() const { return meta_[2]; }
+    int input_c() const { return meta_[3]; }
+    int num_classes() const { return meta_[4]; }
+    const spcv_cu_model* handle() const { return h_; }
+
+    /// run_network over `images` HWC images in device memory: d_input
+    /// [images][H][W][C] -> d_logits [images][num_classes], asynchronous on
+    /// `stream`. strict = bit-identical to the reference executor.
+    void forward(const float* d_input, int images, float* d_logits, bool strict = true,
+                 void* stream = nullptr) const;
+
+private:
+    spcv_cu_model* h_ = nullptr;
+    int meta_[5] = {0, 0, 0, 0, 0};
+};
+
+/// run_network(net, ws, input) for one host HWC image (netdef.cpp:456): copy
+/// in, forward on the device, copy the logits out. Input checks as
+/// check_run_inputs (netdef.cpp:433-441): ShapeError.
+std::vector<float> run_network(const DeviceModel& model, const Tensor& input, bool strict = true);
+
 /// Throws the reference exception class matching an spcv_status code.
 void throw_status(int status, const char* message);
 

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <string_view>
 
@@ -25,6 +26,12 @@ void throw_status(int status, const char* message) {
         case SPCV_ERR_SHAPE: throw ShapeError(msg);
         case SPCV_ERR_FORMAT: throw FormatError(msg);
         case SPCV_ERR_INVALID: throw std::invalid_argument(msg);
+        case SPCV_ERR_MODEL_IO: throw ModelIoError(msg);
+        case SPCV_ERR_BAD_MAGIC: throw BadMagicError(msg);
+        case SPCV_ERR_VERSION: throw UnsupportedVersionError(msg);
+        case SPCV_ERR_TRUNCATED: throw TruncatedError(msg);
+        case SPCV_ERR_CHECKSUM: throw ChecksumError(msg);
+        case SPCV_ERR_MODEL_FORMAT: throw ModelFormatError(msg);
         default: throw DeviceError(msg.empty() ? "spcv_cu: device failure" : msg);
     }
 }
@@ -315,6 +322,78 @@ void spmm_batched_into(const DeviceBcsr& w, const float* d_act, int images, int 
                             d_bias, d_bias ? static_cast<std::size_t>(rows) : 0, act_kind(fused),
                             fused.lo, fused.hi, d_out, SPCV_LAYOUT_CHW, rows, height, width, cfg.m,
                             cfg.n, cfg.strict ? SPCV_MODE_STRICT : SPCV_MODE_FAST, stream));
+}
+
+}  // namespace spcv
+
+namespace spcv {
+
+// ------------------------------------------------------------ model files
+
+DeviceModel::DeviceModel(std::span<const std::uint8_t> bytes) {
+    check(spcv_cu_model_load(bytes.data(), bytes.size(), &h_));
+    int n = 0;
+    check(spcv_cu_model_parse(bytes.data(), bytes.size(), &n));
+    int first[12], last[12];
+    check(spcv_cu_model_layer(h_, 0, first));
+    check(spcv_cu_model_layer(h_, n - 1, last));
+    // info = {kind, cin, cout, in_h, in_w, out_h, out_w, sparse, block_h, act, residual, stride}
+    meta_[0] = n;
+    meta_[1] = first[3];
+    meta_[2] = first[4];
+    meta_[3] = first[1];
+    meta_[4] = last[2];
+}
+
+DeviceModel DeviceModel::load(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw ModelIoError("cannot open model file '" + path + "'");
+    std::vector<std::uint8_t> bytes;
+    std::uint8_t buf[1 << 16];
+    std::size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) bytes.insert(bytes.end(), buf, buf + n);
+    const bool err = std::ferror(f) != 0;
+    std::fclose(f);
+    if (err) throw ModelIoError("error reading model file '" + path + "'");
+    return DeviceModel(std::span<const std::uint8_t>(bytes));
+}
+
+DeviceModel::~DeviceModel() { spcv_cu_model_free(h_); }
+
+void DeviceModel::forward(const float* d_input, int images, float* d_logits, bool strict,
+                          void* stream) const {
+    check(spcv_cu_model_forward(h_, d_input, images, input_h(), input_w(), input_c(), d_logits,
+                                strict ? SPCV_MODE_STRICT : SPCV_MODE_FAST, stream));
+}
+
+std::vector<float> run_network(const DeviceModel& model, const Tensor& input, bool strict) {
+    if (input.layout != Layout::HWC || input.channels != model.input_c() ||
+        input.height != model.input_h() || input.width != model.input_w())
+        throw ShapeError("run: input must be HWC " + std::to_string(model.input_h()) + "x" +
+                         std::to_string(model.input_w()) + "x" + std::to_string(model.input_c()));
+    std::vector<float> logits(static_cast<std::size_t>(model.num_classes()));
+    float *din = nullptr, *dout = nullptr;
+    auto ck = [&](cudaError_t e) {
+        if (e != cudaSuccess) {
+            cudaFree(din);
+            cudaFree(dout);
+            throw DeviceError(std::string("run_network: ") + cudaGetErrorString(e));
+        }
+    };
+    ck(cudaMalloc(&din, input.data.size() * sizeof(float)));
+    ck(cudaMalloc(&dout, logits.size() * sizeof(float)));
+    ck(cudaMemcpy(din, input.data.data(), input.data.size() * sizeof(float), cudaMemcpyHostToDevice));
+    try {
+        model.forward(din, 1, dout, strict, nullptr);
+    } catch (...) {
+        cudaFree(din);
+        cudaFree(dout);
+        throw;
+    }
+    ck(cudaMemcpy(logits.data(), dout, logits.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    cudaFree(din);
+    cudaFree(dout);
+    return logits;
 }
 
 }  // namespace spcv
