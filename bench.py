@@ -460,6 +460,14 @@ def main():
                     "share_of_step": round(dom["share"], 3),
                     "step_hbm_frac": round(bytes_step / (ms_step * 1e-3) / 1e9 / hbm_peak, 4),
                     "gather_roof_tflops": round(gather_roof, 2),
+                    # SURVEY.md §8d "Cap": the best HBM fraction the binding roof allows for
+                    # this layer (t_HBM / max(t_HBM, t_gather), gather roof x block height)
+                    "attainable_frac": round(min(1.0, (dom["alg_bytes"] / (hbm_peak * 1e9)) /
+                                                 max(dom["alg_bytes"] / (hbm_peak * 1e9),
+                                                     dom["flops"] / (gather_roof * 1e12 * dom["bh"]))), 4),
+                    "frac_of_attainable": round((dom["gbs"] / hbm_peak) / min(1.0, (dom["alg_bytes"] / (hbm_peak * 1e9)) /
+                                                max(dom["alg_bytes"] / (hbm_peak * 1e9),
+                                                    dom["flops"] / (gather_roof * 1e12 * dom["bh"]))), 4),
                     "gather_frac": round(dom["gflops"] / 1e3 / gather_roof, 4),
                     "step_gather_frac": round(value / 1e3 / dist.world / gather_roof, 4),
                     "note": "achieved = SURVEY.md §8d algorithmic bytes / CUDA-event launch time. "
