@@ -539,6 +539,29 @@ def bench_network(args, dev, stream, dist, batch):
     ms_fast, _ = timed(m, False, x, steps)
     ms_dense, _ = timed(md, False, x, steps)
     ms_b1, _ = timed(m, True, x[:1], 20)
+    # batch-1 latency with the forward's launches captured once as a CUDA graph
+    ms_b1_graph = None
+    try:
+        x1 = x[:1].clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            m.forward(x1, True, stream)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                y1 = m.forward(x1, True, stream)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(50):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms_b1_graph = round(e0.elapsed_time(e1) / 50, 4)
+        del g, y1
+    except Exception as e:  # noqa: BLE001
+        log(f"network graph capture unavailable: {e!r}"[:200])
     log(f"network MBv1-1.0 x{batch}: strict {ms_strict:.3f} ms, fast {ms_fast:.3f} ms, "
         f"dense(cuBLAS) {ms_dense:.3f} ms, batch-1 latency {ms_b1:.3f} ms")
     out = {"model": "MobileNet-v1-1.0 @224x224x3: entry conv, 13 depthwise + 13 sparse 1x1 (90%, "
@@ -548,7 +571,8 @@ def bench_network(args, dev, stream, dist, batch):
            "ms_per_batch": round(ms_strict, 3), "fast_ms_per_batch": round(ms_fast, 3),
            "dense_cublas_ms_per_batch": round(ms_dense, 3),
            "sparse_speedup_vs_dense": round(ms_dense / ms_fast, 2),
-           "batch1_latency_ms": round(ms_b1, 3), "gpu_launches_per_forward": launches,
+           "batch1_latency_ms": round(ms_b1, 3), "batch1_latency_graph_ms": ms_b1_graph,
+           "gpu_launches_per_forward": launches,
            "how": "spcv_cu_model_forward: every activation device-resident; strict = bit-exact "
                   "with the reference run_network (tests/test_model_files.py)"}
     if dist.world == 1 and not args.no_cpu:

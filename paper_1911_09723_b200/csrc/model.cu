@@ -295,6 +295,10 @@ void free_model(spcv_cu_model* m) {
     for (float* p : m->d_dense) cudaFree(p);
     for (float* p : m->d_bias) cudaFree(p);
     for (float* p : m->d_conv) cudaFree(p);
+    if (m->pool) {
+        cudaDeviceSynchronize();  // no forward may still hold workspace
+        cudaMemPoolDestroy(m->pool);
+    }
     delete m;
 }
 
@@ -375,6 +379,16 @@ extern "C" int spcv_cu_model_load(const uint8_t* bytes, size_t size, spcv_cu_mod
                 e = cudaMemcpy(m->d_bias[i], L.bias.data(), L.bias.size() * 4, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) rc = cuda_fail(e, "model: bias upload");
         }
+    }
+    if (rc == SPCV_OK) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = m->device;
+        cudaError_t e = cudaMemPoolCreate(&m->pool, &props);
+        uint64_t keep = ~0ull;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(m->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        if (e != cudaSuccess) rc = cuda_fail(e, "model: workspace pool");
     }
     if (rc != SPCV_OK) {
         free_model(m);

@@ -50,5 +50,8 @@ struct spcv_cu_model {
     std::vector<float*> d_dense;      // per layer: dense row-major matrix (or null)
     std::vector<float*> d_bias;       // per layer: bias (or null)
     std::vector<float*> d_conv;       // per layer: entry conv [co][ky][kx][ci] / depthwise [c][9]
+    // forward() workspace: a stream-ordered pool owned by the model that keeps
+    // its memory between calls (no re-mapping per forward)
+    cudaMemPool_t pool = nullptr;
 };
 

@@ -357,7 +357,7 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
     // Stream-ordered workspace: two ping-pong buffers + one per residual source.
     std::vector<float*> owned;
     auto alloc = [&](size_t bytes, float** p) -> int {
-        SPCV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 4), st));
+        SPCV_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 4), m->pool, st));
         owned.push_back(*p);
         return SPCV_OK;
     };
