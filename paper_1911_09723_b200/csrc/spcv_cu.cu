@@ -476,6 +476,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.hi = hi;
     a.tail_start = 0x7FFFFFFFFFFFFFFFLL;
     a.tail_split = 1;
+    a.one2 = 0x3f8000003f800000ULL;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
     const int sms = props_for(dev).sms;

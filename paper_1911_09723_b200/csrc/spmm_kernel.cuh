@@ -66,6 +66,9 @@ struct KernelArgs {
     // the last, partial wave of tiles still covers every SM.
     long long tail_start;
     int tail_split;
+    // {1.0f, 1.0f} as f32x2, passed at run time so ptxas cannot fold the
+    // strict pair mul.rn.f32x2 + fma.rn.f32x2(acc, one, p) into one FFMA2.
+    unsigned long long one2;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -105,6 +108,33 @@ __device__ __forceinline__ float madd(float acc, float w, float a) {
         return fmaf(w, a, acc);
     }
 }
+
+// Two columns at once (f32x2: half the FP issue slots of scalar math).
+// Strict: p = w*x rounded, then fma(acc, 1.0, p) = acc + p rounded once,
+// identical to __fadd_rn(acc, __fmul_rn(w, x)) per column (acc*1 is exact).
+// Fast: one fused FFMA2. Used where FP issue binds: block heights >= 2
+// (each activation load feeds BH rows); for BH = 1 the kernel is bound by
+// shared-memory wavefronts and the pairs only add register moves (measured).
+template <bool STRICT>
+__device__ __forceinline__ void madd2(float& ax, float& ay, float w, float xx, float xy,
+                                      unsigned long long one2) {
+    if constexpr (STRICT) {
+        asm("{\n .reg .b64 a, x, p, w2;\n mov.b64 a, {%0, %1};\n mov.b64 x, {%3, %4};\n"
+            " mov.b64 w2, {%2, %2};\n mul.rn.f32x2 p, w2, x;\n fma.rn.f32x2 a, a, %5, p;\n"
+            " mov.b64 {%0, %1}, a;\n}"
+            : "+f"(ax), "+f"(ay)
+            : "f"(w), "f"(xx), "f"(xy), "l"(one2));
+    } else {
+        asm("{\n .reg .b64 a, x, w2;\n mov.b64 a, {%0, %1};\n mov.b64 x, {%3, %4};\n"
+            " mov.b64 w2, {%2, %2};\n fma.rn.f32x2 a, w2, x, a;\n mov.b64 {%0, %1}, a;\n}"
+            : "+f"(ax), "+f"(ay)
+            : "f"(w), "f"(xx), "f"(xy));
+    }
+}
+
+#ifndef SPCV_PAIRED_MIN_BH
+#define SPCV_PAIRED_MIN_BH 2
+#endif
 
 // Activation::apply (tensor.hpp:90-96): ternary compare, NaN and -0.0 pass.
 __device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi) {
@@ -288,10 +318,15 @@ struct Exec {
                 const float w = __uint_as_float(cur.v[t * BH + i]);
 #pragma unroll
                 for (int j = 0; j < NF; ++j) {
-                    acc[i][j].x = madd<STRICT>(acc[i][j].x, w, x[j].x);
-                    acc[i][j].y = madd<STRICT>(acc[i][j].y, w, x[j].y);
-                    acc[i][j].z = madd<STRICT>(acc[i][j].z, w, x[j].z);
-                    acc[i][j].w = madd<STRICT>(acc[i][j].w, w, x[j].w);
+                    if constexpr (BH >= SPCV_PAIRED_MIN_BH) {
+                        madd2<STRICT>(acc[i][j].x, acc[i][j].y, w, x[j].x, x[j].y, a.one2);
+                        madd2<STRICT>(acc[i][j].z, acc[i][j].w, w, x[j].z, x[j].w, a.one2);
+                    } else {
+                        acc[i][j].x = madd<STRICT>(acc[i][j].x, w, x[j].x);
+                        acc[i][j].y = madd<STRICT>(acc[i][j].y, w, x[j].y);
+                        acc[i][j].z = madd<STRICT>(acc[i][j].z, w, x[j].z);
+                        acc[i][j].w = madd<STRICT>(acc[i][j].w, w, x[j].w);
+                    }
                 }
             }
         }
