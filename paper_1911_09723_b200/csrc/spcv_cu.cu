@@ -498,8 +498,17 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
         key.m_out = a.M_out;
         key.sms = sms;
         jit_geometry(key);
+        // The k-major variant is persistent (one CTA per SM, 64 columns per warp
+        // group): with fewer than ~SMs/4 groups the tile kernel's finer tiles win
+        // (measured: c1, 784 columns, 24 vs 17 us; MBv1 pw3 at batch 1, 3136
+        // columns, still faster as k-major).
+        static const long long min_cols_env = [] {
+            const char* e = std::getenv("SPCV_JIT_KMAJOR_MIN_COLS");
+            return e ? std::atoll(e) : -1LL;
+        }();
+        const long long kmajor_min_cols = min_cols_env >= 0 ? min_cols_env : 64LL * sms / 4;
         if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key))
-            return jit_launch(v, a, st);
+            if (v->direct || N >= kmajor_min_cols) return jit_launch(v, a, st);
     }
     switch (w->block_h) {
         case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);

@@ -8,6 +8,10 @@ for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")):
     if p not in sys.path:
         sys.path.insert(0, p)
 
+# The k-major JIT variant serves large column counts only in production; the
+# parity tests' small batches must still exercise it (read once per process).
+os.environ.setdefault("SPCV_JIT_KMAJOR_MIN_COLS", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs the CUDA path")

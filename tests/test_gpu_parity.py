@@ -524,6 +524,7 @@ def test_jit_and_tile_small_k_bit_exact(oracle, monkeypatch, kernel, case):
     rows and one-channel matrices included)."""
     monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
     monkeypatch.setenv("SPCV_JIT_MAX_SEGS", "48")  # exercise multi-segment plans too
+    # (SPCV_JIT_KMAJOR_MIN_COLS=0 for this process: conftest.py)
     _, layer, images = case
     d = make_layer_data(layer, images, 99)
     dw = sp.DeviceBcsr(d.weights)
