@@ -698,3 +698,27 @@ def test_jit_variants_compile_concurrently(oracle):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("kernel", ["jit", "tile"])
+def test_signed_zeros_and_padding_are_bit_exact(oracle, monkeypatch, kernel):
+    """-0.0 biases, -0.0 stored weights, zero activations of both signs and a
+    clamp at lo = -0.0: the order of additions decides the sign of zero
+    results, and every kernel must reproduce the reference bit for bit."""
+    import torch
+
+    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    rng = np.random.default_rng(17)
+    K, M, H, W = 24, 16, 4, 4
+    dense = np.zeros((M, K), np.float32)
+    for r in range(M):
+        cols = rng.choice(K, size=1 + r % 5, replace=False)
+        dense[r, cols] = rng.choice([-1.0, 1.0, -0.5, 2.0, -0.0], size=cols.size).astype(np.float32)
+    m = sp.encode_bcsr(dense, 1)
+    act = rng.choice([0.0, -0.0, 1.0, -1.0], size=(2, K, H, W)).astype(np.float32)
+    bias = rng.choice([0.0, -0.0, 0.5], size=M).astype(np.float32)
+    dw = sp.DeviceBcsr(m)
+    for fused in (NONE, sp.Activation.clamp(-0.0, 6.0), RELU6):
+        got = run_device(m, act, bias, fused, dw=dw)
+        want = oracle.spmm(m, act, bias, fused).reshape(got.shape)
+        assert np.array_equal(bits(got), bits(want)), fused
