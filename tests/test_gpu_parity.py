@@ -722,3 +722,31 @@ def test_signed_zeros_and_padding_are_bit_exact(oracle, monkeypatch, kernel):
         got = run_device(m, act, bias, fused, dw=dw)
         want = oracle.spmm(m, act, bias, fused).reshape(got.shape)
         assert np.array_equal(bits(got), bits(want)), fused
+
+
+@pytest.mark.parametrize("kernel", ["jit", "tile"])
+def test_randomized_shapes_bit_exact(oracle, monkeypatch, kernel):
+    """Seeded random layers (K 1..200, M 1..96, block heights 1/2/4, odd and
+    even spatial sizes, 1-3 images, 0-99 % sparsity, bias or none, clamp or
+    none) through spcv_cu_spmm_into: bit-exact against the oracle for both the
+    weight-specialised and the tile kernel."""
+    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    monkeypatch.setenv("SPCV_JIT_MAX_SEGS", "48")
+    rng = np.random.default_rng(2024)
+    for case in range(14):
+        bh = int(rng.choice([1, 2, 4]))
+        K = int(rng.integers(1, 201))
+        M = int(rng.integers(1, 25)) * bh
+        H, W = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        B = int(rng.integers(1, 4))
+        sparsity = float(rng.choice([0.0, 0.5, 0.9, 0.99]))
+        dense = (rng.standard_normal((M, K)) * 0.3).astype(np.float32)
+        dense[rng.random((M // bh, K)).repeat(bh, axis=0) < sparsity] = 0
+        m = sp.encode_bcsr(dense, bh)
+        act = rng.uniform(-1, 1, (B, K, H, W)).astype(np.float32)
+        bias = rng.uniform(-1, 1, M).astype(np.float32) if case % 3 else None
+        fused = RELU6 if case % 2 else NONE
+        dw = sp.DeviceBcsr(m)
+        got = run_device(m, act, bias, fused, dw=dw)
+        want = oracle.spmm(m, act, bias, fused).reshape(got.shape)
+        assert np.array_equal(bits(got), bits(want)), (case, K, M, bh, H, W, B, sparsity)
