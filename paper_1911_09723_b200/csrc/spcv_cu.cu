@@ -635,7 +635,30 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
     // Image chunks of ~kHostChunkBytes; each chunk: H2D -> kernel -> D2H.
     const size_t per_image = S * (static_cast<size_t>(act_c) + out_c) * sizeof(float);
     const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(images, host_chunk_bytes() / std::max<size_t>(per_image, 1))));
-    const int nchunks = images > 0 ? (images + chunk - 1) / chunk : 0;
+    // Chunk schedule: ramp up (1/8, 1/4, 1/2 of a full chunk) so the first
+    // kernel starts early, full chunks in the middle, ramp down at the end so
+    // the last download is short: the pipeline's fill and drain shrink.
+    std::vector<int> sizes;
+    {
+        const bool ramp = std::getenv("SPCV_HOST_RAMP") == nullptr || std::atoi(std::getenv("SPCV_HOST_RAMP")) != 0;
+        int left = images;
+        std::vector<int> tail;
+        if (ramp && images >= 4 * chunk) {
+            for (int f : {8, 4, 2}) {
+                const int n = std::max(1, chunk / f);
+                sizes.push_back(n);
+                tail.push_back(n);
+                left -= 2 * n;
+            }
+        }
+        while (left > 0) {
+            const int n = std::min(chunk, left);
+            sizes.push_back(n);
+            left -= n;
+        }
+        sizes.insert(sizes.end(), tail.rbegin(), tail.rend());  // 1/2, 1/4, 1/8 of a chunk
+    }
+    const int nchunks = static_cast<int>(sizes.size());
     while (static_cast<int>(hs.ev_in.size()) < nchunks) {
         cudaEvent_t a = nullptr, b = nullptr;
         SPCV_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -646,8 +669,8 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
     const size_t in_img = S * act_c, out_img = S * out_c;
     if (n_bias)
         SPCV_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice, hs.h2d));
-    for (int c = 0; c < nchunks; ++c) {
-        const int i0 = c * chunk, ni = std::min(chunk, images - i0);
+    for (int c = 0, i0 = 0; c < nchunks; i0 += sizes[c], ++c) {
+        const int ni = sizes[c];
         SPCV_CUDA(cudaMemcpyAsync(d_act + i0 * in_img, act + i0 * in_img, ni * in_img * sizeof(float),
                                   cudaMemcpyHostToDevice, hs.h2d));
         SPCV_CUDA(cudaEventRecord(hs.ev_in[c], hs.h2d));
