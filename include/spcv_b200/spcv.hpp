@@ -114,6 +114,32 @@ struct BcsrMatrix {
 };
 
 /// encode_bcsr / decode_bcsr (sparse.cpp:108-148): host-side preparation.
+/// sparse.hpp:20-28: tile shape of a sparsity mask.
+struct BlockConfig {
+    int out_block = 1;
+    int in_block = 1;
+    explicit BlockConfig(int ob = 1, int ib = 1);
+};
+
+/// sparse.hpp:30-57: bit-packed keep mask over a rows x cols matrix (row-major).
+struct SparsityMask {
+    int rows = 0;
+    int cols = 0;
+    std::vector<std::uint64_t> bits;
+    SparsityMask() = default;
+    SparsityMask(int r, int c);
+    bool get(int r, int c) const;
+    void set(int r, int c, bool v);
+    std::int64_t popcount() const;
+};
+
+/// sparse.cpp:63-98: zero llround(tiles * sparsity) whole tiles chosen by a
+/// partial Fisher-Yates shuffle with std::mt19937(seed); same checks.
+SparsityMask generate_mask(int rows, int cols, double sparsity, BlockConfig block,
+                           std::uint32_t seed);
+/// sparse.cpp:100-106.
+void apply_mask(DenseMatrix& w, const SparsityMask& mask);
+
 BcsrMatrix encode_bcsr(const DenseMatrix& w, int block_h);
 DenseMatrix decode_bcsr(const BcsrMatrix& m);
 

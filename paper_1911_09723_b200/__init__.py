@@ -16,6 +16,7 @@ from .spmm import (
     parse_model_status,
     Activation,
     BcsrMatrix,
+    BlockConfig,
     DeviceBcsr,
     DeviceError,
     FormatError,
@@ -28,7 +29,9 @@ from .spmm import (
     decode_bcsr,
     default_strip_width,
     dense_gemm_batched_into,
+    apply_mask,
     encode_bcsr,
+    generate_mask,
     parse_tier,
     parse_variant,
     resolve_tier,
@@ -44,7 +47,7 @@ from .spmm import (
 __all__ = [
     "BadMagicError", "ChecksumError", "DeviceModel", "ModelFormatError", "ModelIoError",
     "TruncatedError", "UnsupportedVersionError", "parse_model_status",
-    "Activation", "BcsrMatrix", "dense_gemm_batched_into", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
+    "Activation", "BcsrMatrix", "BlockConfig", "apply_mask", "generate_mask", "dense_gemm_batched_into", "DeviceBcsr", "DeviceError", "FormatError", "Layout",
     "LayoutError", "MicrokernelConfig", "ShapeError", "Tensor", "Tier", "decode_bcsr",
     "default_strip_width", "encode_bcsr", "parse_tier", "parse_variant", "resolve_tier",
     "spconv_1x1", "spmm", "spmm_batched_into", "spmm_host_batched", "spmm_into", "spmm_layer",

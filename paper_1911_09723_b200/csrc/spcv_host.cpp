@@ -13,7 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
+#include <random>
 #include <string_view>
 
 namespace spcv {
@@ -394,6 +396,71 @@ std::vector<float> run_network(const DeviceModel& model, const Tensor& input, bo
     cudaFree(din);
     cudaFree(dout);
     return logits;
+}
+
+// ------------------------------------------------------------ masks
+
+BlockConfig::BlockConfig(int ob, int ib) : out_block(ob), in_block(ib) {
+    if ((ob != 1 && ob != 2 && ob != 4) || (ib != 1 && ib != 2 && ib != 4))
+        throw FormatError("block sizes must be 1, 2 or 4");
+}
+
+SparsityMask::SparsityMask(int r, int c)
+    : rows(r), cols(c), bits((static_cast<std::size_t>(r) * c + 63) / 64, 0) {
+    if (r < 1 || c < 1) throw ShapeError("mask dims must be >= 1");
+}
+
+bool SparsityMask::get(int r, int c) const {
+    const std::size_t i = static_cast<std::size_t>(r) * cols + c;
+    return (bits[i >> 6] >> (i & 63)) & 1u;
+}
+
+void SparsityMask::set(int r, int c, bool v) {
+    const std::size_t i = static_cast<std::size_t>(r) * cols + c;
+    const std::uint64_t m = std::uint64_t{1} << (i & 63);
+    bits[i >> 6] = v ? (bits[i >> 6] | m) : (bits[i >> 6] & ~m);
+}
+
+std::int64_t SparsityMask::popcount() const {
+    std::int64_t n = 0;
+    for (std::uint64_t w : bits) n += __builtin_popcountll(w);
+    return n;
+}
+
+SparsityMask generate_mask(int rows, int cols, double sparsity, BlockConfig block,
+                           std::uint32_t seed) {
+    if (sparsity < 0.0 || sparsity >= 1.0) throw std::invalid_argument("sparsity must be in [0, 1)");
+    if (rows % block.out_block != 0) throw FormatError("generate_mask: rows not divisible by out_block");
+    if (cols % block.in_block != 0) throw FormatError("generate_mask: cols not divisible by in_block");
+    const int tcols = cols / block.in_block;
+    const std::size_t tiles = static_cast<std::size_t>(rows / block.out_block) * tcols;
+    const std::size_t zeroed = static_cast<std::size_t>(std::llround(static_cast<double>(tiles) * sparsity));
+    // tile order after a partial shuffle: only the first `zeroed` positions matter
+    std::vector<std::uint32_t> order(tiles);
+    for (std::size_t i = 0; i < tiles; ++i) order[i] = static_cast<std::uint32_t>(i);
+    std::mt19937 gen(seed);
+    for (std::size_t i = 0; i < zeroed && i + 1 < tiles; ++i) {
+        std::uniform_int_distribution<std::size_t> pick(i, tiles - 1);
+        std::swap(order[i], order[pick(gen)]);
+    }
+    SparsityMask mask(rows, cols);
+    for (auto& w : mask.bits) w = ~std::uint64_t{0};
+    const std::size_t total = static_cast<std::size_t>(rows) * cols;
+    if (total % 64) mask.bits.back() &= (std::uint64_t{1} << (total % 64)) - 1;  // unused tail bits clear
+    for (std::size_t i = 0; i < zeroed; ++i) {
+        const int tr = static_cast<int>(order[i] / tcols), tc = static_cast<int>(order[i] % tcols);
+        for (int dr = 0; dr < block.out_block; ++dr)
+            for (int dc = 0; dc < block.in_block; ++dc)
+                mask.set(tr * block.out_block + dr, tc * block.in_block + dc, false);
+    }
+    return mask;
+}
+
+void apply_mask(DenseMatrix& w, const SparsityMask& mask) {
+    if (w.rows != mask.rows || w.cols != mask.cols) throw ShapeError("apply_mask: matrix/mask shape mismatch");
+    for (int r = 0; r < w.rows; ++r)
+        for (int c = 0; c < w.cols; ++c)
+            if (!mask.get(r, c)) w.data[static_cast<std::size_t>(r) * w.cols + c] = 0.0f;
 }
 
 }  // namespace spcv

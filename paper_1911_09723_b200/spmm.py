@@ -251,6 +251,84 @@ class BcsrMatrix:
                 raise FormatError("bcsr: column indices not strictly increasing")
 
 
+@dataclass
+class BlockConfig:
+    """sparse.hpp:20-28: tile shape of the mask (out_block x in_block, each 1, 2 or 4)."""
+
+    out_block: int = 1
+    in_block: int = 1
+
+    def __post_init__(self):
+        if self.out_block not in (1, 2, 4) or self.in_block not in (1, 2, 4):
+            raise FormatError("block sizes must be 1, 2 or 4")
+
+
+class _Mt19937:
+    """std::mt19937 seeded with a 32-bit value (numpy's legacy MT19937 seeding
+    is the same init_genrand), raw 32-bit draws."""
+
+    def __init__(self, seed: int):
+        self._rs = np.random.RandomState(int(seed) & 0xFFFFFFFF)
+
+    def __call__(self) -> int:
+        return int(self._rs.randint(0, 2**32, dtype=np.uint64))
+
+
+def _uniform_size_t(draw, a: int, b: int) -> int:
+    """std::uniform_int_distribution<size_t>(a, b) over a 32-bit engine as
+    libstdc++ 13 implements it: Lemire's nearly divisionless downscaling with
+    a 64-bit product when the range fits the engine's 32 bits."""
+    urange = b - a
+    if urange >= 0xFFFFFFFF:
+        raise ValueError("range beyond 32 bits is not needed for masks")
+    r = urange + 1
+    prod = draw() * r
+    low = prod & 0xFFFFFFFF
+    if low < r:
+        threshold = ((-r) & 0xFFFFFFFF) % r
+        while low < threshold:
+            prod = draw() * r
+            low = prod & 0xFFFFFFFF
+    return a + (prod >> 32)
+
+
+def generate_mask(rows: int, cols: int, sparsity: float, block: BlockConfig = BlockConfig(),
+                  seed: int = 0) -> np.ndarray:
+    """sparse.cpp:63-98: keep-mask [rows][cols] (True = kept) with exactly
+    llround(tiles * sparsity) whole out_block x in_block tiles zeroed, chosen
+    by a partial Fisher-Yates shuffle driven by std::mt19937(seed). Same
+    checks and order: sparsity in [0, 1) (ValueError), divisibility (FormatError)."""
+    if not (0.0 <= sparsity < 1.0):
+        raise ValueError("sparsity must be in [0, 1)")
+    if rows % block.out_block:
+        raise FormatError("generate_mask: rows not divisible by out_block")
+    if cols % block.in_block:
+        raise FormatError("generate_mask: cols not divisible by in_block")
+    if rows < 1 or cols < 1:
+        raise ShapeError("mask dims must be >= 1")
+    trows, tcols = rows // block.out_block, cols // block.in_block
+    tiles = trows * tcols
+    zeroed = int(np.floor(tiles * sparsity + 0.5))  # llround of a non-negative value
+    pos = list(range(tiles))
+    draw = _Mt19937(seed)
+    for i in range(min(zeroed, tiles - 1)):
+        j = _uniform_size_t(draw, i, tiles - 1)
+        pos[i], pos[j] = pos[j], pos[i]
+    keep_t = np.ones(tiles, dtype=bool)
+    keep_t[np.asarray(pos[:zeroed], dtype=np.int64)] = False
+    keep = keep_t.reshape(trows, tcols)
+    return np.repeat(np.repeat(keep, block.out_block, axis=0), block.in_block, axis=1)
+
+
+def apply_mask(w: np.ndarray, keep: np.ndarray) -> np.ndarray:
+    """sparse.cpp:100-106: zero the pruned positions (ShapeError on mismatch)."""
+    if w.shape != keep.shape:
+        raise ShapeError("apply_mask: matrix/mask shape mismatch")
+    out = np.array(w, dtype=np.float32, copy=True)
+    out[~keep] = 0.0
+    return out
+
+
 def encode_bcsr(w: np.ndarray, block_h: int) -> BcsrMatrix:
     """sparse.cpp:108-134: keep a block iff any member != 0 (so -0.0 is zero)."""
     if block_h not in (1, 2, 4):

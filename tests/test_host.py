@@ -149,6 +149,44 @@ def test_jit_direct_variant_source(monkeypatch):
     assert rows_seen == list(range(10))
 
 
+MASK_CASES = [(8, 8, 0.5, 2, 1, 1234), (10, 1, 0.25, 1, 1, 5), (4, 4, 0.0, 1, 1, 5), (4, 4, 0.999, 1, 1, 5),
+              (16, 12, 0.7, 4, 2, 77), (64, 64, 0.9, 1, 1, 42), (64, 32, 0.8, 4, 1, 9),
+              (128, 128, 0.8, 1, 1, 3), (512, 512, 0.9, 4, 1, 11), (30, 30, 0.5, 4, 1, 1), (8, 8, 1.0, 1, 1, 1)]
+
+
+def test_generate_mask_mirrors_match_reference(ref):
+    """generate_mask (sparse.cpp:63-98) in the Python and C++ mirrors: the same
+    keep bits as the compiled reference (std::mt19937 + libstdc++'s
+    uniform_int_distribution), the same errors, test_sparse.cpp popcounts."""
+    exe = os.path.join(ROOT, "tests", "cpp", "test_mask")
+    r = subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include",
+                        os.path.join(ROOT, "tests", "cpp", "test_mask.cpp"), "-o", exe,
+                        f"-L{LIBDIR}", "-lspcv_b200", "-lspcv_cu", f"-Wl,-rpath,{LIBDIR}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    args = [str(v) for case in MASK_CASES for v in case]
+    out = subprocess.run([exe] + args, capture_output=True, text=True).stdout.split("\n")
+    os.remove(exe)
+    for (rows, cols, s, ob, ib, seed), line in zip(MASK_CASES, out):
+        rc, want = ref.generate_mask(rows, cols, s, ob, ib, seed)
+        if rc != 0:  # reference rejected: both mirrors reject with the mapped error
+            assert line in ("FormatError", "invalid_argument")
+            with pytest.raises((sp.FormatError, ValueError)):
+                sp.generate_mask(rows, cols, s, sp.BlockConfig(ob, ib), seed)
+            continue
+        got_py = sp.generate_mask(rows, cols, s, sp.BlockConfig(ob, ib), seed)
+        assert np.array_equal(got_py, want), (rows, cols, s, ob, ib, seed)
+        pop, bits_ = line.split()
+        got_cpp = np.frombuffer(bits_.encode(), dtype=np.uint8).reshape(rows, cols) == ord("1")
+        assert np.array_equal(got_cpp, want) and int(pop) == int(want.sum())
+    assert [int(l.split()[0]) for l in out[:4]] == [32, 7, 16, 0]  # test_sparse.cpp:73-104
+    w = np.ones((4, 4), np.float32)
+    keep = sp.generate_mask(4, 4, 0.5, sp.BlockConfig(), 1)
+    assert np.array_equal(sp.apply_mask(w, keep) != 0, keep)
+    with pytest.raises(sp.ShapeError):
+        sp.apply_mask(np.ones((3, 4), np.float32), keep)
+
+
 def test_cpp_dropin_library_exports_reference_api():
     so = os.path.join(LIBDIR, "libspcv_b200.so")
     out = subprocess.run(["nm", "-DC", so], capture_output=True, text=True).stdout
