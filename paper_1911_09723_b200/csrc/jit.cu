@@ -47,14 +47,14 @@ using namespace spcv_detail;
 namespace {
 
 constexpr int kKC = 32;        // channels per staged chunk
-constexpr int kCols = 64;      // columns per warp group (2 per lane)
-constexpr int kRowsMax = 64;   // rows per segment (2 accumulator registers each)
+constexpr int kRowsMax = 128;  // rows per segment
 
-// Rows a segment may hold so that its accumulator pairs fit the register
-// budget of a W-warp CTA (65536 / (32 W), at most 255) with ~48 to spare.
-int rows_max(int warps) {
+// Rows a segment may hold so that its accumulators (cpl registers per row:
+// columns per lane) fit the register budget of a W-warp CTA (65536 / (32 W),
+// at most 255) with ~48 to spare.
+int rows_max(int warps, int cpl) {
     const int regs = std::min(255, 65536 / (32 * warps));
-    return std::max(8, std::min(kRowsMax, (regs - 48) / 2));
+    return std::max(8, std::min(kRowsMax / cpl, (regs - 48) / cpl));
 }
 
 int env_int(const char* name, int dflt) {
@@ -96,7 +96,7 @@ bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& 
     cur.instr = fixed;
     for (int r = 0; r < rows; ++r) {
         const long long c = static_cast<long long>(per_weight) * row_nnz(row_ptr, BH, r) + 10;
-        if (cur.r1 > cur.r0 && (cur.instr + c > budget || cur.r1 - cur.r0 == rows_max(key.warps))) {
+        if (cur.r1 > cur.r0 && (cur.instr + c > budget || cur.r1 - cur.r0 == rows_max(key.warps, key.cpl))) {
             segs.push_back(cur);
             cur = Segment();
             cur.r0 = cur.r1 = r;
@@ -137,6 +137,10 @@ bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& 
 std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
                        const float* values, const JitKey& key, const std::vector<Segment>& segs) {
     const int nkc = (K + kKC - 1) / kKC;
+    const int C = key.cpl;             // columns per lane: 2 (f32x2) or 1 (scalar)
+    const int kCols = 32 * C;          // columns per warp group
+    const int Q = kCols / 4;           // 16 B quads per staged channel row
+    const int RPI = 32 / Q;            // channel rows one warp-wide copy covers
     std::ostringstream o;
     o << "#define K " << K << "LL\n#define KC " << kKC << "\n#define NKC " << nkc
       << "\n#define W " << key.warps << "\n#define P " << key.stages << "\n"
@@ -145,6 +149,7 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
          " return (unsigned)__cvta_generic_to_shared(p); }\n"
       << "#define CP16(d, off, s) asm volatile(\"cp.async.cg.shared.global [%0+\" #off \"], [%1], 16;\" :: \"r\"(d), \"l\"(s) : \"memory\")\n"
       << "#define LDS64(v, a, off) asm volatile(\"ld.shared.b64 %0, [%1+\" #off \"];\" : \"=l\"(v) : \"r\"(a))\n"
+      << "#define LDS32(v, a, off) asm volatile(\"ld.shared.f32 %0, [%1+\" #off \"];\" : \"=f\"(v) : \"r\"(a))\n"
       << "__device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 d;"
          " asm(\"mul.rn.f32x2 %0, %1, %2;\" : \"=l\"(d) : \"l\"(a), \"l\"(b)); return d; }\n"
       << "__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 d;"
@@ -201,25 +206,25 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
           << "  const long long ng = first < G ? (G - first + stride - 1) / stride : 0;\n"
           << "  long long ig = 0; int ikc = 0; bool valid = false; const float* src = nullptr;\n"
           << "  auto set_src = [&](long long gi) {\n"
-          << "    const long long nq = (first + gi * stride) * " << kCols << " + 4 * (lane & 15);\n"
+          << "    const long long nq = (first + gi * stride) * " << kCols << " + 4 * (lane % " << Q << ");\n"
           << "    valid = gi < ng && nq < N;\n"
           << "    if (valid) { const long long b = nq / S, s = nq - b * S;"
-             " src = act + b * K * S + s + (lane >> 4) * S; }\n"
+             " src = act + b * K * S + s + (lane / " << Q << ") * S; }\n"
           << "  };\n"
           << "  const unsigned ring_sa = sa(ring);\n"
           << "  int islot = 0, cslot = 0;\n"
           << "  auto issue = [&]() {\n"
-          << "    const unsigned dst = ring_sa + islot * (KC * " << kCols * 4 << ") + ((lane >> 4) * "
-          << kCols << " + 4 * (lane & 15)) * 4;\n"
+          << "    const unsigned dst = ring_sa + islot * (KC * " << kCols * 4 << ") + ((lane / " << Q << ") * "
+          << kCols << " + 4 * (lane % " << Q << ")) * 4;\n"
           << "    if (valid) {\n"
           << "      const float* sk = src + (long long)ikc * KC * S;\n";
-        for (int j = 0; j < kKC / 2; ++j) {
-            const std::string cp = "CP16(dst, " + std::to_string(2 * j * kCols * 4) + ", sk + " +
-                                   std::to_string(2 * j) + "LL * S);";
+        for (int j = 0; j < kKC / RPI; ++j) {
+            const std::string cp = "CP16(dst, " + std::to_string(RPI * j * kCols * 4) + ", sk + " +
+                                   std::to_string(RPI * j) + "LL * S);";
             if (K % kKC == 0)
                 o << "      " << cp << "\n";
             else
-                o << "      if (ikc * KC + (lane >> 4) + " << 2 * j << " < K) " << cp << "\n";
+                o << "      if (ikc * KC + (lane / " << Q << ") + " << RPI * j << " < K) " << cp << "\n";
         }
         o << "    }\n"
           << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n"
@@ -233,27 +238,46 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
           << "  for (long long gi = 0; gi < ng; ++gi) {\n";
         for (int q = 0; q < R; ++q) {
             const int r = sg.r0 + q;
-            o << "    u64 a" << q << " = " << (key.bias ? "dup(__ldg(bias + " + std::to_string(r) + "))" : "0ULL")
-              << ";\n";
+            if (C == 2)
+                o << "    u64 a" << q << " = " << (key.bias ? "dup(__ldg(bias + " + std::to_string(r) + "))" : "0ULL")
+                  << ";\n";
+            else
+                o << "    float a" << q << " = " << (key.bias ? "__ldg(bias + " + std::to_string(r) + ")" : "0.0f")
+                  << ";\n";
         }
         for (int kc = 0; kc < nkc; ++kc) {
             o << "    issue();\n"
               << "    asm volatile(\"cp.async.wait_group %0;\" :: \"n\"(P - 1) : \"memory\");\n"
               << "    __syncwarp();\n"
-              << "    { const unsigned xs = ring_sa + cslot * (KC * " << kCols * 4 << ") + 8 * lane;\n";
+              << "    { const unsigned xs = ring_sa + cslot * (KC * " << kCols * 4 << ") + " << 4 * C
+              << " * lane;\n";
             for (int k = kc * kKC; k < std::min(K, (kc + 1) * kKC); ++k) {
                 if (by_k[k].empty()) continue;
-                o << "      { u64 x; LDS64(x, xs, " << (k - kc * kKC) * kCols * 4 << ");\n";
+                if (C == 2)
+                    o << "      { u64 x; LDS64(x, xs, " << (k - kc * kKC) * kCols * 4 << ");\n";
+                else
+                    o << "      { float x; LDS32(x, xs, " << (k - kc * kKC) * kCols * 4 << ");\n";
                 for (const auto& [q, v] : by_k[k]) {
-                    if (key.strict)
+                    if (C == 1) {
+                        uint32_t u;
+                        std::memcpy(&u, &v, 4);
+                        char wv[40];
+                        std::snprintf(wv, sizeof wv, "__uint_as_float(0x%08xu)", u);
+                        if (key.strict)
+                            o << "        a" << q << " = __fadd_rn(a" << q << ", __fmul_rn(" << wv << ", x));\n";
+                        else
+                            o << "        a" << q << " = __fmaf_rn(" << wv << ", x, a" << q << ");\n";
+                    } else if (key.strict) {
                         o << "        a" << q << " = fma2(a" << q << ", one, mul2(" << imm2(v) << ", x));\n";
-                    else
+                    } else {
                         o << "        a" << q << " = fma2(" << imm2(v) << ", x, a" << q << ");\n";
+                    }
                 }
                 o << "      }\n";
             }
             o << "    }\n    __syncwarp();\n    if (++cslot == P) cslot = 0;\n";
         }
+        if (C == 2) {
         o << "    const long long n0 = (first + gi * stride) * " << kCols << " + 2 * lane;\n"
           << "    if (n0 < N) {\n"
           << "      const long long b = n0 / S, s = n0 - b * S;\n"
@@ -271,6 +295,21 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
                      " v.x = __fadd_rn(v.x, t.x); v.y = __fadd_rn(v.y, t.y); }\n";
             o << "        __stcs(op, v); op += S2; }  // row " << sg.r0 + q << "\n";
         }
+        } else {
+        o << "    const long long n0 = (first + gi * stride) * " << kCols << " + lane;\n"
+          << "    if (n0 < N) {\n"
+          << "      const long long b = n0 / S, s = n0 - b * S;\n"
+          << "      const int S1 = (int)S;\n"
+          << "      float* op = out + (b * " << key.m_out << "LL + " << sg.r0 << ") * S + s;\n";
+        if (key.res)
+            o << "      const float* rp = res + (b * " << key.m_out << "LL + " << sg.r0 << ") * S + s;\n";
+        for (int q = 0; q < R; ++q) {
+            o << "      { float v = a" << q << ";\n";
+            if (key.clamp) o << "        v = clampf(v, lo, hi);\n";
+            if (key.res) o << "        v = __fadd_rn(v, __ldcs(rp)); rp += S1;\n";
+            o << "        __stcs(op, v); op += S1; }  // row " << sg.r0 + q << "\n";
+        }
+        }
         o << "    }\n  }\n}\n";
     }
     o << "extern \"C\" __global__ void __launch_bounds__(W * 32, 1)"
@@ -279,7 +318,7 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
          " const float* __restrict__ res, u64 one) {\n"
       << "  extern __shared__ float4 smem4[];\n"
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-      << "  float* ring = reinterpret_cast<float*>(smem4) + warp * (P * KC * " << kCols << ");\n"
+      << "  float* ring = reinterpret_cast<float*>(smem4) + warp * (P * KC * " << 32 * key.cpl << ");\n"
       << "  const int seg = seg_of[blockIdx.x], rank = rank_of[blockIdx.x];\n"
       << "  switch (seg) {\n";
     for (size_t si = 0; si < segs.size(); ++si)
@@ -363,7 +402,7 @@ std::string gen_direct(int M, int K, int BH, const uint32_t* row_ptr, const uint
 // Which generator serves (matrix, key): direct for small K within the code
 // budget, else the k-major segmented kernel when the layout allows it.
 enum class JitKind { kNone, kDirect, kKMajor };
-JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key,
+JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key,
                     std::vector<Segment>& segs) {
     // fast mode (1 FFMA per weight) affords the direct variant up to K = 128
     // (measured: MBv1 pw3 in the full step 2.387 -> 2.326 ms); strict keeps
@@ -372,7 +411,27 @@ JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, const JitKey&
     if (K <= direct_maxk &&
         direct_instr(M, K, BH, row_ptr, key) <= env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr))
         return JitKind::kDirect;
-    if (key.vec && plan_segments(M, K, BH, row_ptr, key, segs)) return JitKind::kKMajor;
+    if (!key.vec) return JitKind::kNone;
+    // k-major: 2 columns per lane (f32x2), or 1 column per lane (scalar, twice
+    // the rows per segment) when that fits the matrix in a single segment:
+    // every extra segment re-reads the activations (measured, MBv1 pw3 in the
+    // full step: 240 -> 199 us; two 1-column segments lose to the tile kernel)
+    JitKey k2 = key, k1 = key;
+    k2.cpl = 2;
+    k1.cpl = 1;
+    std::vector<Segment> s2, s1;
+    const bool ok2 = plan_segments(M, K, BH, row_ptr, k2, s2);
+    const bool ok1 = plan_segments(M, K, BH, row_ptr, k1, s1);
+    if (ok1 && s1.size() == 1 && (!ok2 || s2.size() > 1)) {
+        segs = s1;  // a single segment reads the activations once
+        key.cpl = 1;
+        return JitKind::kKMajor;
+    }
+    if (ok2) {
+        segs = s2;
+        key.cpl = 2;
+        return JitKind::kKMajor;
+    }
     return JitKind::kNone;
 }
 
@@ -412,15 +471,17 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     JitVariant& v = w->jit.back();
     v.key = key;
     std::vector<Segment> segs;
-    const JitKind kind = choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), key, segs);
+    JitKey gk = key;  // plus the generator's choices (columns per lane)
+    const JitKind kind = choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), gk, segs);
     if (kind == JitKind::kNone) return nullptr;  // the tile kernel runs
     v.direct = kind == JitKind::kDirect;
+    v.cpl = gk.cpl;
     std::vector<char> cubin;
     const std::string src =
         v.direct ? gen_direct(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
                               w->h_values.data(), key)
                  : gen_source(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
-                              w->h_values.data(), key, segs);
+                              w->h_values.data(), gk, segs);
     if (jit_compile(src, cubin) != SPCV_OK) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&v.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
@@ -432,7 +493,7 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     if (e == cudaSuccess && !v.direct)
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 jit_smem_bytes(key.warps, key.stages));
+                                 jit_smem_bytes(key.warps, key.stages, v.cpl));
     if (e != cudaSuccess) {
         cuda_fail(e, "jit: kernel setup");
         cudaLibraryUnload(v.lib);
@@ -478,7 +539,7 @@ int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st)
     }
     SPCV_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(v->fn), dim3(v->key.sms),
                                dim3(v->key.warps * 32), args,
-                               jit_smem_bytes(v->key.warps, v->key.stages), st));
+                               jit_smem_bytes(v->key.warps, v->key.stages, v->cpl), st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }

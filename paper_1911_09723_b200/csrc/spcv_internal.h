@@ -23,6 +23,7 @@ struct JitKey {
     int m_out = 0;
     int sms = 0;
     int warps = 8, stages = 3;  // CTA geometry (jit_geometry)
+    int cpl = 2;                // k-major columns per lane (generator's choice; not part of the key)
     bool operator==(const JitKey& o) const {
         return strict == o.strict && clamp == o.clamp && bias == o.bias && res == o.res &&
                vec == o.vec && m_out == o.m_out && sms == o.sms && warps == o.warps &&
@@ -34,6 +35,7 @@ struct JitVariant {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t fn = nullptr;  // null: not built (ineligible, or compile/load failed)
     bool direct = false;        // one thread per column (small K) vs k-major segments
+    int cpl = 2;                // k-major: columns per lane (2 = f32x2, 1 = scalar)
     int segments = 0;
 };
 
@@ -93,7 +95,7 @@ constexpr int kJitMaxSegs = 2;      // segments per matrix (more: i-cache misses
 constexpr int kJitDirectMaxK = 64;  // direct variant: activations of a column in registers
 constexpr int kJitWarps = 8;
 constexpr int kJitStages = 3;
-inline int jit_smem_bytes(int warps, int stages) { return warps * stages * 32 * 64 * 4; }
+inline int jit_smem_bytes(int warps, int stages, int cpl = 2) { return warps * stages * 32 * 32 * cpl * 4; }
 void jit_geometry(JitKey& key);  // warps/stages (SPCV_JIT_WARPS / SPCV_JIT_STAGES override)
 const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
 int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st);

@@ -76,15 +76,18 @@ def _jit_terms(src):
             continue
         if line.strip() == "issue();":
             kc += 1
-        m = re.search(r"LDS64\(x, xs, (\d+)\)", line)
-        if m:
-            k = kc * 32 + int(m.group(1)) // 256
+        m = re.search(r"LDS(64|32)\(x, xs, (\d+)\)", line)
+        if m:  # offset = channel-in-chunk x columns per group (64 or 32) x 4 B
+            k = kc * 32 + int(m.group(2)) // (256 if m.group(1) == "64" else 128)
         m = re.search(r"a(\d+) = fma2\(a\d+, one, mul2\(0x([0-9a-f]{8})[0-9a-f]{8}ULL, x\)\)", line)
         if m:
             terms.setdefault((seg, int(m.group(1))), []).append((k, int(m.group(2), 16), "strict"))
         m = re.search(r"a(\d+) = fma2\(0x([0-9a-f]{8})[0-9a-f]{8}ULL, x, a\d+\)", line)
         if m:
             terms.setdefault((seg, int(m.group(1))), []).append((k, int(m.group(2), 16), "fast"))
+        m = re.search(r"a(\d+) = __fadd_rn\(a\d+, __fmul_rn\(__uint_as_float\(0x([0-9a-f]{8})u\), x\)\)", line)
+        if m:  # one column per lane (scalar) k-major variant
+            terms.setdefault((seg, int(m.group(1))), []).append((k, int(m.group(2), 16), "strict"))
     return terms
 
 
@@ -120,6 +123,25 @@ def test_jit_kernel_source_and_nvrtc_compile_without_gpu(monkeypatch):
                 q += 1
                 r += 1
         assert r == m_out
+
+
+def test_jit_single_segment_one_column_per_lane(monkeypatch):
+    """A 128-row matrix that needs two 2-column segments fits one segment at one
+    column per lane: the planner picks it (activations read once), and every
+    row's terms are still its stored weights in ascending channel order."""
+    monkeypatch.delenv("SPCV_JIT_SEG_INSTR", raising=False)
+    monkeypatch.delenv("SPCV_JIT_MAX_SEGS", raising=False)
+    rng = np.random.default_rng(9)
+    dense = rng.standard_normal((128, 128)).astype(np.float32)
+    dense[rng.random((128, 128)) < 0.9] = 0
+    m = sp.encode_bcsr(dense, 1)
+    rc, src, cubin, nseg = _jit_compile(m, _capi.MODE_STRICT)
+    assert rc == 0 and nseg == 1 and "LDS32(" in src and "LDS64(" not in src.split("void seg0")[1]
+    rp, ci, va = np.asarray(m.row_ptr), np.asarray(m.col_idx), np.asarray(m.values)
+    terms = _jit_terms(src)
+    for r in range(128):
+        want = [(int(ci[b]), int(va[b].view(np.uint32)), "strict") for b in range(rp[r], rp[r + 1])]
+        assert terms.get((0, r), []) == want, r
 
 
 def test_jit_direct_variant_source(monkeypatch):
