@@ -498,17 +498,21 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
         key.m_out = a.M_out;
         key.sms = sms;
         jit_geometry(key);
-        // The k-major variant is persistent (one CTA per SM, 64 columns per warp
-        // group): with fewer than ~SMs/4 groups the tile kernel's finer tiles win
-        // (measured: c1, 784 columns, 24 vs 17 us; MBv1 pw3 at batch 1, 3136
-        // columns, still faster as k-major).
+        // The k-major variant is persistent (one CTA per SM, 32 or 64 columns
+        // per warp group, each segment on its share of the SMs): with fewer
+        // column groups than its warps the tile kernel's finer tiles win
+        // (measured: c1, 784 columns, 24 vs 17 us; MBv2 384->64 @14x14 x128,
+        // 25088 columns in 2 segments, 53 vs 38 us).
         static const long long min_cols_env = [] {
             const char* e = std::getenv("SPCV_JIT_KMAJOR_MIN_COLS");
             return e ? std::atoll(e) : -1LL;
         }();
-        const long long kmajor_min_cols = min_cols_env >= 0 ? min_cols_env : 64LL * sms / 4;
-        if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key))
-            if (v->direct || N >= kmajor_min_cols) return jit_launch(v, a, st);
+        if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key)) {
+            const long long min_cols =
+                min_cols_env >= 0 ? min_cols_env
+                                  : 32LL * v->cpl * sms * key.warps / std::max(1, v->segments);
+            if (v->direct || N >= min_cols) return jit_launch(v, a, st);
+        }
     }
     switch (w->block_h) {
         case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);
