@@ -244,33 +244,43 @@ def main():
 
     # The same step replayed as one CUDA graph (the 13 launches captured once):
     # launch overhead out of the way, which matters for the batch-1 configs.
+    # Every rank reaches the same collectives whether or not its capture works
+    # (a failure is reported as -1 and the max over ranks tells every rank).
     graph = None
-    try:
-        if args.no_alt:
-            raise RuntimeError("skipped (--no-alt)")
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            step()  # every kernel variant exists before capture
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=stream):
-                step()
-            g.replay()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            dist.barrier(dev)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            for _ in range(args.steps):
+    if not args.no_alt:
+        ms_local, err = -1.0, ""
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                step()  # every kernel variant exists before capture
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=stream):
+                    step()
                 g.replay()
-            e1.record(stream)
-            torch.cuda.synchronize()
-        ms_graph = dist.max(e0.elapsed_time(e1), device=torch.device("cuda", dev)) / args.steps
-        graph = {"ms_per_step": round(ms_graph, 4),
-                 "value": round(dist.sum(flops_step, device=torch.device("cuda", dev)) / (ms_graph * 1e-3) / 1e9, 3),
-                 "how": "torch.cuda.CUDAGraph capture of one step (13 spcv_cu_spmm_into launches), replayed"}
+                torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 - reported, the eager number stands
+            g, err = None, repr(e)[:200]
+        flag = 1.0 if g is not None else -1.0
+        ok = -dist.max(-flag, device=torch.device("cuda", dev)) > 0  # min over ranks: all captured
+        if ok:
+            with torch.cuda.stream(stream):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                dist.barrier(dev)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                for _ in range(args.steps):
+                    g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize()
+            ms_local = e0.elapsed_time(e1)
+        ms_graph = dist.max(ms_local, device=torch.device("cuda", dev)) / args.steps if ok else -1.0
+        if ok:
+            graph = {"ms_per_step": round(ms_graph, 4),
+                     "value": round(dist.sum(flops_step, device=torch.device("cuda", dev)) / (ms_graph * 1e-3) / 1e9, 3),
+                     "how": "torch.cuda.CUDAGraph capture of one step (13 spcv_cu_spmm_into launches), replayed"}
+        else:
+            graph = {"unavailable": err or "capture failed on another rank"}
         del g
-    except Exception as e:  # noqa: BLE001 - reported, the eager number stands
-        graph = {"unavailable": repr(e)[:200]}
 
     # The other arithmetic mode on the same packed weights (reported beside the
     # headline, which is the mode selected by --mode): strict = bit-exact,
