@@ -217,6 +217,15 @@ void spmm_batched_into(const DeviceBcsr& w, const float* d_act, int images, int 
                        const float* d_bias, const Activation& fused, float* d_out,
                        const MicrokernelConfig& cfg = {}, void* stream = nullptr);
 
+/// The executor's pointwise step (run_network, netdef.cpp:494-512) on device
+/// tensors: `w` may carry up to block_h-1 padded rows beyond `out_channels`
+/// (computed, never stored), `d_bias` has out_channels entries (or nullptr),
+/// and `d_residual` (nullptr or [images][out_channels][H*W]) is added after the
+/// activation. Asynchronous on `stream`.
+void spmm_layer(const DeviceBcsr& w, const float* d_act, int images, int height, int width,
+                const float* d_bias, const Activation& fused, const float* d_residual, float* d_out,
+                int out_channels, bool strict = true, void* stream = nullptr);
+
 // ------------------------------------------------------------ model files
 /// model_io.hpp:13-41: the model-file error family.
 class ModelIoError : public std::runtime_error {

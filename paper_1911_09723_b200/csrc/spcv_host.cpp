@@ -330,6 +330,16 @@ void spmm_batched_into(const DeviceBcsr& w, const float* d_act, int images, int 
 
 namespace spcv {
 
+void spmm_layer(const DeviceBcsr& w, const float* d_act, int images, int height, int width,
+                const float* d_bias, const Activation& fused, const float* d_residual, float* d_out,
+                int out_channels, bool strict, void* stream) {
+    check(spcv_cu_spmm_layer(w.handle(), d_act, images, w.cols(), height, width, d_bias,
+                             d_bias ? static_cast<size_t>(out_channels) : 0,
+                             fused.kind == Activation::Kind::Clamp ? SPCV_ACT_CLAMP : SPCV_ACT_NONE,
+                             fused.lo, fused.hi, d_residual, d_out, out_channels,
+                             strict ? SPCV_MODE_STRICT : SPCV_MODE_FAST, stream));
+}
+
 // ------------------------------------------------------------ model files
 
 DeviceModel::DeviceModel(std::span<const std::uint8_t> bytes) {

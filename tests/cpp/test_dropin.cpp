@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "spcv_b200/spcv.hpp"
 
 using namespace spcv;
@@ -198,6 +200,49 @@ int main() {
         const BcsrMatrix back = dw.unpack();
         CHECK(back.row_ptr == m.row_ptr && back.col_idx == m.col_idx && back.values == m.values);
         std::puts("ok device_pack_roundtrip");
+    }
+    {  // run_network's pointwise step (netdef.cpp:494-512): padded rows, residual after the clamp
+        std::mt19937 rng(41);
+        const int rows = 10, K = 24, H = 6, W = 5, B = 2, S = H * W;
+        DenseMatrix w = random_matrix(rows + 2, K, rng);  // 2 padded rows (block height 4)
+        for (int c = 0; c < K; ++c) w(rows, c) = w(rows + 1, c) = 0.0f;
+        const BcsrMatrix m = masked(w, 0.6, 4, rng);
+        DenseMatrix logical(rows, K);
+        const DenseMatrix dec = decode_bcsr(m);
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < K; ++c) logical(r, c) = dec(r, c);
+        std::vector<float> act(static_cast<std::size_t>(B) * K * S), res(static_cast<std::size_t>(B) * rows * S);
+        for (float& v : act) v = static_cast<float>(rng() % 1000) / 999.0f;
+        for (float& v : res) v = static_cast<float>(rng() % 2000) / 999.0f - 1.0f;
+        const std::vector<float> bias = random_bias(rows, rng);
+        float *da = nullptr, *db = nullptr, *dr = nullptr, *dout = nullptr;
+        cudaMalloc(&da, act.size() * 4);
+        cudaMalloc(&db, bias.size() * 4);
+        cudaMalloc(&dr, res.size() * 4);
+        cudaMalloc(&dout, res.size() * 4);
+        cudaMemcpy(da, act.data(), act.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(db, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(dr, res.data(), res.size() * 4, cudaMemcpyHostToDevice);
+        DeviceBcsr dw(m);
+        spmm_layer(dw, da, B, H, W, db, Activation::relu6(), dr, dout, rows);
+        std::vector<float> got(res.size());
+        cudaMemcpy(got.data(), dout, got.size() * 4, cudaMemcpyDeviceToHost);
+        bool same = true;
+        for (int b = 0; b < B; ++b) {
+            Tensor img(K, H, W, Layout::CHW);
+            std::copy(act.begin() + b * K * S, act.begin() + (b + 1) * K * S, img.data.begin());
+            const std::vector<float> want = dense_ref(logical, img, bias, Activation::relu6());
+            for (int i = 0; i < rows * S; ++i) {
+                const float v = want[i] + res[static_cast<std::size_t>(b) * rows * S + i];
+                same = same && got[static_cast<std::size_t>(b) * rows * S + i] == v;
+            }
+        }
+        CHECK(same);
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dr);
+        cudaFree(dout);
+        std::puts("ok spmm_layer_padded_residual");
     }
     std::printf("all %d checks passed\n", g_checks);
     return 0;

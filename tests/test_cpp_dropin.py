@@ -12,8 +12,9 @@ SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
 
 def build(tmp_path):
     exe = str(tmp_path / "test_dropin")
-    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", f"-I{ROOT}/include", SRC, "-o", exe,
-           f"-L{LIB}", "-lspcv_b200", "-lspcv_cu", f"-Wl,-rpath,{LIB}"]
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", f"-I{ROOT}/include", "-I/usr/local/cuda/include",
+           SRC, "-o", exe, f"-L{LIB}", "-lspcv_b200", "-lspcv_cu", f"-Wl,-rpath,{LIB}",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     return exe
