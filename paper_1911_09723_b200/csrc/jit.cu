@@ -338,26 +338,60 @@ long long direct_instr(int M, int K, int BH, const uint32_t* row_ptr, const JitK
     long long weights = 0;
     const int rows = std::min(M, key.m_out);
     for (int r = 0; r < rows; ++r) weights += row_nnz(row_ptr, BH, r);
-    return (key.strict ? 2 : 1) * weights + K + 6LL * rows;
+    return (key.strict ? 2 : 1) * weights + K + 6LL * rows + (key.dw ? 30LL * K : 0);
 }
 
 std::string gen_direct(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
                        const float* values, const JitKey& key) {
     std::ostringstream o;
+    auto imm = [](float v) {
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        char wv[40];
+        std::snprintf(wv, sizeof wv, "__uint_as_float(0x%08xu)", u);
+        return std::string(wv);
+    };
     o << "extern \"C\" __global__ void __launch_bounds__(128) spcv_jit(const float* __restrict__ act,"
          " float* __restrict__ out, const float* __restrict__ bias, long long N, long long S,"
-         " float lo, float hi, const float* __restrict__ res, unsigned long long one) {\n"
+         " float lo, float hi, const float* __restrict__ res, unsigned long long one,"
+         " const float* __restrict__ dwin, int H, int W, int OW, int pt, int pl, float dlo, float dhi) {\n"
       << "  const long long n = blockIdx.x * 128LL + threadIdx.x;\n"
       << "  if (n >= N) return;\n"
       << "  const long long b = n / S, s = n - b * S;\n"
-      << "  const float* a = act + b * " << K << "LL * S + s;\n"
       << "  float* o = out + b * " << key.m_out << "LL * S + s;\n";
     if (key.res) o << "  const float* rp = res + b * " << key.m_out << "LL * S + s;\n";
     std::vector<char> used(static_cast<size_t>(K), 0);
     const int brows = M / BH;
     for (uint32_t b = 0; b < row_ptr[brows]; ++b) used[col_idx[b]] = 1;
-    for (int k = 0; k < K; ++k)
-        if (used[k]) o << "  const float x" << k << " = __ldcs(a + " << k << "LL * S);\n";
+    if (!key.dw) {
+        o << "  const float* a = act + b * " << K << "LL * S + s;\n";
+        for (int k = 0; k < K; ++k)
+            if (used[k]) o << "  const float x" << k << " = __ldcs(a + " << k << "LL * S);\n";
+    } else {
+        // x_k = the depthwise output (channel k, this pixel): bias first, taps
+        // in (ky, kx) order, out-of-image taps skipped, ternary clamp
+        // (depthwise_conv_chw, kernels.cpp:385-422)
+        o << "  const int oy = (int)(s / OW), ox = (int)(s - (long long)oy * OW);\n"
+          << "  const int iy0 = oy * " << key.dw_stride << " - pt, ix0 = ox * " << key.dw_stride << " - pl;\n"
+          << "  const long long HW = (long long)H * W;\n"
+          << "  const float* din = dwin + b * " << K << "LL * HW;\n";
+        for (int t = 0; t < 9; ++t)
+            o << "  const bool v" << t << " = (unsigned)(iy0 + " << t / 3 << ") < (unsigned)H && (unsigned)(ix0 + "
+              << t % 3 << ") < (unsigned)W;\n"
+              << "  const long long q" << t << " = v" << t << " ? (long long)(iy0 + " << t / 3 << ") * W + (ix0 + "
+              << t % 3 << ") : 0;\n";
+        for (int k = 0; k < K; ++k) {
+            if (!used[k]) continue;
+            o << "  float x" << k << " = " << (key.dw_b ? imm(key.dw_b[k]) : std::string("0.0f")) << ";\n"
+              << "  { const float* dk = din + " << k << "LL * HW;\n";
+            for (int t = 0; t < 9; ++t)
+                o << "    if (v" << t << ") x" << k << " = __fadd_rn(x" << k << ", __fmul_rn("
+                  << imm(key.dw_w[static_cast<size_t>(k) * 9 + t]) << ", __ldg(dk + q" << t << ")));\n";
+            if (key.dw_clamp)
+                o << "    x" << k << " = x" << k << " < dlo ? dlo : (x" << k << " > dhi ? dhi : x" << k << ");\n";
+            o << "  }\n";
+        }
+    }
     constexpr int kIL = 4;
     const int rows = std::min(M, key.m_out);
     for (int r0 = 0; r0 < rows; r0 += kIL) {
@@ -411,7 +445,7 @@ JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key,
     if (K <= direct_maxk &&
         direct_instr(M, K, BH, row_ptr, key) <= env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr))
         return JitKind::kDirect;
-    if (!key.vec) return JitKind::kNone;
+    if (!key.vec || key.dw) return JitKind::kNone;
     // k-major: 2 columns per lane (f32x2), or 1 column per lane (scalar, twice
     // the rows per segment) when that fits the matrix in a single segment:
     // every extra segment re-reads the activations (measured, MBv1 pw3 in the
@@ -520,7 +554,7 @@ void jit_release(spcv_cu_weights* w) {
     w->jit.clear();
 }
 
-int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st) {
+int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st, const JitDwArgs* dw) {
     long long N = a.N, S = a.S;
     float lo = a.lo, hi = a.hi;
     const float* act = a.act;
@@ -528,7 +562,9 @@ int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st)
     const float* bias = a.bias;
     const float* res = a.residual;
     unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
-    void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res, &one};
+    JitDwArgs d = dw ? *dw : JitDwArgs{};
+    void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res, &one,
+                    &d.in, &d.H, &d.W, &d.OW, &d.pad_t, &d.pad_l, &d.lo, &d.hi};
     if (v->direct) {
         const long long blocks = (N + 127) / 128;
         if (blocks > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "jit: grid too large");

@@ -382,6 +382,39 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
     constexpr int kT = 256;
     for (size_t i = 0; i < n && rc == SPCV_OK; ++i) {
         const Layer& L = net.layers[i];
+        // Depthwise -> sparse 1x1 pair (opt-in, SPCV_FUSE_DW=1): the 1x1 layer's
+        // weight-specialised kernel computes the depthwise outputs it needs
+        // itself (same arithmetic order), so the depthwise activation never goes
+        // through HBM. Measured slower than two kernels on MBv1 (spcv_cu.cu).
+        if (L.kind == kDepthwise && i + 1 < n && !save[i] && L.residual_src < 0 &&
+            net.layers[i + 1].kind == kPointwise && m->w[i + 1] && (L.stride == 1 || L.stride == 2)) {
+            const Layer& P = net.layers[i + 1];
+            const Pad ph = same_pad(L.in_h, 3, L.stride), pw = same_pad(L.in_w, 3, L.stride);
+            JitDwArgs dwa;
+            dwa.in = cur;
+            dwa.H = L.in_h;
+            dwa.W = L.in_w;
+            dwa.OW = pw.out;
+            dwa.pad_t = ph.before;
+            dwa.pad_l = pw.before;
+            dwa.lo = L.lo;
+            dwa.hi = L.hi;
+            float* pdst = i + 2 == n ? logits : (save[i + 1] ? saved[i + 1] : (cur == ping[0] ? ping[1] : ping[0]));
+            const float* pres = P.residual_src >= 0 ? saved[static_cast<size_t>(P.residual_src)] : nullptr;
+            const int frc = spmm_dw_fused(m->w[i + 1], dwa, L.stride, L.other.data(),
+                                          L.bias.empty() ? nullptr : L.bias.data(), L.act_kind == 1, images,
+                                          ph.out, pw.out, m->d_bias[i + 1], P.act_kind, P.lo, P.hi, pres, pdst,
+                                          P.cout, mode, st);
+            if (frc == SPCV_OK) {
+                cur = pdst;
+                ++i;
+                continue;
+            }
+            if (frc != SPCV_ERR_UNSUPPORTED) {
+                rc = frc;
+                break;
+            }
+        }
         float* dst = i + 1 == n ? logits : (save[i] ? saved[i] : (cur == ping[0] ? ping[1] : ping[0]));
         const long long out_elems = static_cast<long long>(images) * L.cout * L.out_h * L.out_w;
         const float* res = L.residual_src >= 0 ? saved[static_cast<size_t>(L.residual_src)] : nullptr;

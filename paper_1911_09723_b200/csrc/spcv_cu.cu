@@ -599,6 +599,55 @@ extern "C" int spcv_cu_spmm_layer(const spcv_cu_weights* w, const float* act, in
                   static_cast<cudaStream_t>(stream), out_c, residual);
 }
 
+namespace spcv_detail {
+
+int spmm_dw_fused(const spcv_cu_weights* w, const JitDwArgs& dw, int dw_stride, const float* dw_w_host,
+                  const float* dw_b_host, bool dw_clamp, int images, int out_h, int out_w,
+                  const float* bias, int act_kind, float lo, float hi, const float* residual,
+                  float* out, int out_c, int mode, cudaStream_t st) {
+    if (!w || !w->jit_eligible) return SPCV_ERR_UNSUPPORTED;
+    // Opt-in (SPCV_FUSE_DW=1): measured slower than the two separate kernels
+    // on MBv1-1.0 (dw1+pw1 507 vs 550 us, dw2+pw2 392 vs 323 us): the fused
+    // producer recomputes each depthwise output per 1x1 column thread and
+    // becomes issue-bound.
+    const char* e = std::getenv("SPCV_FUSE_DW");
+    if (!e || std::atoi(e) == 0) return SPCV_ERR_UNSUPPORTED;
+    const long long S = static_cast<long long>(out_h) * out_w;
+    const long long N = S * images;
+    if (N == 0) return SPCV_OK;
+    int dev = 0;
+    SPCV_CUDA(cudaGetDevice(&dev));
+    if (dev != w->device) return SPCV_ERR_UNSUPPORTED;
+    JitKey key;
+    key.strict = mode == SPCV_MODE_STRICT;
+    key.clamp = act_kind == SPCV_ACT_CLAMP;
+    key.bias = bias != nullptr;
+    key.res = residual != nullptr;
+    key.m_out = out_c;
+    key.sms = props_for(dev).sms;
+    jit_geometry(key);
+    key.dw = true;
+    key.dw_clamp = dw_clamp;
+    key.dw_stride = dw_stride;
+    key.dw_w = dw_w_host;
+    key.dw_b = dw_b_host;
+    const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key);
+    if (!v || !v->direct) return SPCV_ERR_UNSUPPORTED;
+    spcvk::KernelArgs a{};
+    a.out = out;
+    a.bias = bias;
+    a.residual = residual;
+    a.N = N;
+    a.S = static_cast<int>(S);
+    a.M_out = out_c;
+    a.act_kind = act_kind;
+    a.lo = key.clamp ? lo : 0.0f;
+    a.hi = key.clamp ? hi : 0.0f;
+    return jit_launch(v, a, st, &dw);
+}
+
+}  // namespace spcv_detail
+
 extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_layout,
                                       int images, int act_c, int act_h, int act_w,
                                       const float* bias, size_t bias_len, int act_kind, float lo,

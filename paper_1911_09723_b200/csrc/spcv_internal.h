@@ -24,11 +24,25 @@ struct JitKey {
     int sms = 0;
     int warps = 8, stages = 3;  // CTA geometry (jit_geometry)
     int cpl = 2;                // k-major columns per lane (generator's choice; not part of the key)
+    // Fused 3x3 depthwise producer (executor, network.cu): the direct variant
+    // computes its input channels from the depthwise layer's input instead of
+    // loading them; the depthwise weights/bias (host copies) become immediates.
+    bool dw = false, dw_clamp = false;
+    int dw_stride = 1;
+    const float* dw_w = nullptr;  // [K][9] host
+    const float* dw_b = nullptr;  // [K] host or null
     bool operator==(const JitKey& o) const {
         return strict == o.strict && clamp == o.clamp && bias == o.bias && res == o.res &&
                vec == o.vec && m_out == o.m_out && sms == o.sms && warps == o.warps &&
-               stages == o.stages;
+               stages == o.stages && dw == o.dw && dw_clamp == o.dw_clamp &&
+               dw_stride == o.dw_stride && dw_w == o.dw_w && dw_b == o.dw_b;
     }
+};
+// Runtime arguments of a fused depthwise producer.
+struct JitDwArgs {
+    const float* in = nullptr;  // depthwise input [images][K][H][W]
+    int H = 0, W = 0, OW = 1, pad_t = 0, pad_l = 0;
+    float lo = 0.0f, hi = 0.0f;
 };
 struct JitVariant {
     JitKey key;
@@ -98,7 +112,15 @@ constexpr int kJitStages = 3;
 inline int jit_smem_bytes(int warps, int stages, int cpl = 2) { return warps * stages * 32 * 32 * cpl * 4; }
 void jit_geometry(JitKey& key);  // warps/stages (SPCV_JIT_WARPS / SPCV_JIT_STAGES override)
 const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
-int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st);
+int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st,
+               const JitDwArgs* dw = nullptr);
+// Depthwise 3x3 (host copies of its weights/bias) fused into the next sparse
+// 1x1 layer through the direct JIT variant; SPCV_ERR_UNSUPPORTED when that
+// variant does not serve the matrix (the caller then runs the two layers).
+int spmm_dw_fused(const spcv_cu_weights* w, const JitDwArgs& dw, int dw_stride, const float* dw_w_host,
+                  const float* dw_b_host, bool dw_clamp, int images, int out_h, int out_w,
+                  const float* bias, int act_kind, float lo, float hi, const float* residual,
+                  float* out, int out_c, int mode, cudaStream_t st);
 void jit_release(spcv_cu_weights* w);
 
 }  // namespace spcv_detail

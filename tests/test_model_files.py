@@ -164,3 +164,31 @@ def test_device_forward_checks_input_shape(files):
     with pytest.raises(sp.ShapeError):
         m.forward(torch.zeros(1, L0["in_h"] + 1, L0["in_w"], L0["cin"], device="cuda"))
     assert m.forward(torch.zeros(0, L0["in_h"], L0["in_w"], L0["cin"], device="cuda")).shape[0] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mbv1-0.25", "mbv2-0.35", "ours-mbv1-0.25"])
+def test_fused_depthwise_pointwise_matches_unfused(ref, files, monkeypatch, name):
+    """Depthwise layers fused into the next sparse 1x1 layer's weight-specialised
+    kernel (opt-in, SPCV_FUSE_DW=1) give the same bits as running them
+    separately (the default) and as the reference run_network, with fewer
+    launches."""
+    import torch
+
+    data = files[name]
+    L0 = sp.DeviceModel(data).layers[0]
+    x = np.random.default_rng(5).uniform(-1, 1, (2, L0["in_h"], L0["in_w"], L0["cin"])).astype(np.float32)
+    want = ref.run_model(data, x)
+    outs, launches = {}, {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("SPCV_FUSE_DW", fuse)
+        m = sp.DeviceModel(data)
+        xt = torch.from_numpy(x).cuda()
+        m.forward(xt)  # compile every variant first
+        torch.cuda.synchronize()
+        n0 = sp.launch_count()
+        outs[fuse] = m.forward(xt).cpu().numpy()
+        launches[fuse] = sp.launch_count() - n0
+    assert np.array_equal(outs["1"].view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(outs["0"].view(np.uint32), want.view(np.uint32))
+    assert launches["1"] < launches["0"], launches
