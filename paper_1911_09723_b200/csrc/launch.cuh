@@ -131,7 +131,7 @@ int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt,
 template <int BH, int LPR, int NF>
 int launch_s(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
              bool strict, bool vec, cudaStream_t st) {
-    return w->STEPS == 2 ? launch_g<BH, LPR, NF, 2>(a, w, nt, sms, strict, vec, st)
+    return a.steps == 2 ? launch_g<BH, LPR, NF, 2>(a, w, nt, sms, strict, vec, st)
                          : launch_g<BH, LPR, NF, 4>(a, w, nt, sms, strict, vec, st);
 }
 

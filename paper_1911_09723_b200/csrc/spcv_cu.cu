@@ -139,6 +139,8 @@ void free_weights(spcv_cu_weights* w) {
     cudaFree(w->d_values);
     cudaFree(w->d_stream);
     cudaFree(w->d_bin_beg);
+    cudaFree(w->d_stream_fast);
+    cudaFree(w->d_bin_beg_fast);
     jit_release(w);
     delete w;
 }
@@ -197,10 +199,19 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
         return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: too many block rows");
     // Steps per chunk: rows are padded to a multiple of STEPS (zero row,
     // weight -0.0f) and the max over a row group, so short rows (mean < 16
-    // blocks) use 2-step chunks. SPCV_STEPS=2|4 overrides.
-    int STEPS = nblocks < static_cast<size_t>(16) * brows ? 2 : 4;
+    // blocks) use 2-step chunks. Measured per layer (profiles/r1_notes.md):
+    // in strict mode unstructured square/expanding matrices up to 512 rows
+    // also run faster with 2 (MBv1 512x512: 218 -> 207 us) while projections
+    // (rows < cols), 1024-row matrices and block heights 2/4 keep 4; in fast
+    // mode 4 wins for all but short rows (FFMA leaves more issue slots for
+    // the index work). When the two modes differ both streams are packed.
+    // SPCV_STEPS=2|4 overrides both.
+    const bool short_rows = nblocks < static_cast<size_t>(16) * brows;
+    const bool small_square = block_h == 1 && rows <= 512 && rows >= cols;
+    int steps_strict = (short_rows || small_square) ? 2 : 4;
+    int steps_fast = short_rows ? 2 : 4;
     if (const char* e = std::getenv("SPCV_STEPS"))
-        if (std::atoi(e) == 2 || std::atoi(e) == 4) STEPS = std::atoi(e);
+        if (std::atoi(e) == 2 || std::atoi(e) == 4) steps_strict = steps_fast = std::atoi(e);
 
     // paper-format streams
     std::vector<uint32_t> nnz(brows), delta(nblocks);
@@ -222,86 +233,101 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return nnz[a] > nnz[b]; });
     const int ngroups = (brows + G - 1) / G;
-    std::vector<int> gchunks(ngroups);
-    for (int g = 0; g < ngroups; ++g) {
-        uint32_t mx = 0;
-        for (int s = 0; s < G; ++s) {
-            const int k = g * G + s;
-            if (k < brows) mx = std::max(mx, nnz[order[k]]);
-        }
-        gchunks[g] = static_cast<int>((mx + STEPS - 1) / STEPS);
-    }
-    std::vector<std::vector<int>> bins(kBins);
-    using Item = std::tuple<long long, int, int>;  // load, priority, bin
-    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
-    for (int b = 0; b < kBins; ++b) {
-        const int warp = b / kMaxSplit, i = b % kMaxSplit;
-        heap.emplace(0LL, bitrev3(i) * kWarps + warp, b);
-    }
-    std::vector<int> gorder(ngroups);
-    for (int g = 0; g < ngroups; ++g) gorder[g] = g;
-    std::stable_sort(gorder.begin(), gorder.end(),
-                     [&](int a, int b) { return gchunks[a] > gchunks[b]; });
-    for (int g : gorder) {
-        auto [load, prio, b] = heap.top();
-        heap.pop();
-        bins[b].push_back(g);
-        heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
-    }
 
-    // Chunk (spmm_kernel.cuh, Fmt): index area G x STEPS u16 (padded to 16 B),
-    // value area G x STEPS*BH f32 in 16 B units [unit][slot] (8 B per slot
-    // when STEPS*BH == 2). Headers: first index word kHeaderHi | block_row.
-    const int NI = STEPS / 2, NV = STEPS * BH;
-    const size_t IB = (static_cast<size_t>(G) * NI * 4 + 15) / 16 * 16;
-    const size_t CB = IB + static_cast<size_t>(G) * NV * 4;
-    size_t total = 0;
-    for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
-    std::vector<unsigned char> stream(total * CB + 16, 0);
-    std::vector<uint32_t> bin_beg(kBins + 1);
-    size_t cur = 0;
-    auto idx_word = [&](size_t chunk, int slot, int wi) -> uint32_t* {
-        return reinterpret_cast<uint32_t*>(stream.data() + chunk * CB + (slot * NI + wi) * 4);
+    // One execution stream for STEPS steps per chunk.
+    struct Built {
+        std::vector<unsigned char> stream;
+        std::vector<uint32_t> bin_beg;
+        size_t nchunks = 0;
     };
-    auto val_word = [&](size_t chunk, int slot, int f) -> float* {
-        unsigned char* base = stream.data() + chunk * CB + IB;
-        if (NV == 2) return reinterpret_cast<float*>(base + slot * 8 + f * 4);
-        return reinterpret_cast<float*>(base + ((f / 4) * G + slot) * 16 + (f % 4) * 4);
-    };
-    for (int b = 0; b < kBins; ++b) {
-        bin_beg[b] = static_cast<uint32_t>(cur);
-        for (int g : bins[b]) {
-            const int nch = gchunks[g];
+    auto build = [&](int STEPS, Built& out) {
+        std::vector<int> gchunks(ngroups);
+        for (int g = 0; g < ngroups; ++g) {
+            uint32_t mx = 0;
             for (int s = 0; s < G; ++s) {
                 const int k = g * G + s;
-                *idx_word(cur, s, 0) =
-                    spcvk::kHeaderHi | (k < brows ? static_cast<uint32_t>(order[k]) : spcvk::kNoRow);
+                if (k < brows) mx = std::max(mx, nnz[order[k]]);
             }
-            ++cur;
-            for (int c = 0; c < nch; ++c, ++cur) {
+            gchunks[g] = static_cast<int>((mx + STEPS - 1) / STEPS);
+        }
+        std::vector<std::vector<int>> bins(kBins);
+        using Item = std::tuple<long long, int, int>;  // load, priority, bin
+        std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+        for (int b = 0; b < kBins; ++b) {
+            const int warp = b / kMaxSplit, i = b % kMaxSplit;
+            heap.emplace(0LL, bitrev3(i) * kWarps + warp, b);
+        }
+        std::vector<int> gorder(ngroups);
+        for (int g = 0; g < ngroups; ++g) gorder[g] = g;
+        std::stable_sort(gorder.begin(), gorder.end(),
+                         [&](int a, int b) { return gchunks[a] > gchunks[b]; });
+        for (int g : gorder) {
+            auto [load, prio, b] = heap.top();
+            heap.pop();
+            bins[b].push_back(g);
+            heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
+        }
+
+        // Chunk (spmm_kernel.cuh, Fmt): index area G x STEPS u16 (padded to 16 B),
+        // value area G x STEPS*BH f32 in 16 B units [unit][slot] (8 B per slot
+        // when STEPS*BH == 2). Headers: first index word kHeaderHi | block_row.
+        const int NI = STEPS / 2, NV = STEPS * BH;
+        const size_t IB = (static_cast<size_t>(G) * NI * 4 + 15) / 16 * 16;
+        const size_t CB = IB + static_cast<size_t>(G) * NV * 4;
+        size_t total = 0;
+        for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
+        std::vector<unsigned char>& stream = out.stream;
+        stream.assign(total * CB + 16, 0);
+        out.bin_beg.assign(kBins + 1, 0);
+        size_t cur = 0;
+        auto idx_word = [&](size_t chunk, int slot, int wi) -> uint32_t* {
+            return reinterpret_cast<uint32_t*>(stream.data() + chunk * CB + (slot * NI + wi) * 4);
+        };
+        auto val_word = [&](size_t chunk, int slot, int f) -> float* {
+            unsigned char* base = stream.data() + chunk * CB + IB;
+            if (NV == 2) return reinterpret_cast<float*>(base + slot * 8 + f * 4);
+            return reinterpret_cast<float*>(base + ((f / 4) * G + slot) * 16 + (f % 4) * 4);
+        };
+        for (int b = 0; b < kBins; ++b) {
+            out.bin_beg[b] = static_cast<uint32_t>(cur);
+            for (int g : bins[b]) {
+                const int nch = gchunks[g];
                 for (int s = 0; s < G; ++s) {
                     const int k = g * G + s;
-                    const int br = k < brows ? order[k] : -1;
-                    for (int t = 0; t < STEPS; ++t) {
-                        // Padding steps read the zero row K with weight -0.0f, which
-                        // leaves any accumulator bit-identical (see spmm_kernel.cuh).
-                        uint32_t idx = static_cast<uint32_t>(cols);
-                        const uint32_t e = static_cast<uint32_t>(STEPS * c + t);
-                        const bool real = br >= 0 && e < nnz[br];
-                        const uint32_t blk = real ? row_ptr[br] + e : 0;
-                        if (real) idx = col_idx[blk];
-                        uint32_t* w = idx_word(cur, s, t / 2);
-                        *w |= (t & 1) ? (idx << 16) : idx;
-                        for (int i = 0; i < BH; ++i)
-                            *val_word(cur, s, t * BH + i) =
-                                real ? values[static_cast<size_t>(blk) * BH + i] : -0.0f;
+                    *idx_word(cur, s, 0) =
+                        spcvk::kHeaderHi | (k < brows ? static_cast<uint32_t>(order[k]) : spcvk::kNoRow);
+                }
+                ++cur;
+                for (int c = 0; c < nch; ++c, ++cur) {
+                    for (int s = 0; s < G; ++s) {
+                        const int k = g * G + s;
+                        const int br = k < brows ? order[k] : -1;
+                        for (int t = 0; t < STEPS; ++t) {
+                            // Padding steps read the zero row K with weight -0.0f, which
+                            // leaves any accumulator bit-identical (see spmm_kernel.cuh).
+                            uint32_t idx = static_cast<uint32_t>(cols);
+                            const uint32_t e = static_cast<uint32_t>(STEPS * c + t);
+                            const bool real = br >= 0 && e < nnz[br];
+                            const uint32_t blk = real ? row_ptr[br] + e : 0;
+                            if (real) idx = col_idx[blk];
+                            uint32_t* w = idx_word(cur, s, t / 2);
+                            *w |= (t & 1) ? (idx << 16) : idx;
+                            for (int i = 0; i < BH; ++i)
+                                *val_word(cur, s, t * BH + i) =
+                                    real ? values[static_cast<size_t>(blk) * BH + i] : -0.0f;
+                        }
                     }
                 }
             }
         }
-    }
-    bin_beg[kBins] = static_cast<uint32_t>(cur);
-    if (cur > 0xFFFFFFF0ull) return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: stream too large");
+        out.bin_beg[kBins] = static_cast<uint32_t>(cur);
+        out.nchunks = cur;
+    };
+    Built bs, bf;
+    build(steps_strict, bs);
+    if (steps_fast != steps_strict) build(steps_fast, bf);
+    if (bs.nchunks > 0xFFFFFFF0ull || bf.nchunks > 0xFFFFFFF0ull)
+        return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: stream too large");
 
     auto* w = new (std::nothrow) spcv_cu_weights;
     if (!w) return fail(SPCV_ERR_CUDA, "spcv_cu_pack: out of host memory");
@@ -310,12 +336,13 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     w->block_h = block_h;
     w->brows = brows;
     w->G = G;
-    w->STEPS = STEPS;
+    w->STEPS = steps_strict;
+    w->STEPS_fast = steps_fast;
     w->LPR = lay.LPR;
     w->NF = lay.NF;
     w->T = T;
     w->nblocks = nblocks;
-    w->nchunks = cur;
+    w->nchunks = bs.nchunks;
     cudaGetDevice(&w->device);
     // Small-K matrices also get a weight-specialised kernel (jit.cu), compiled
     // on first use. SPCV_JIT=0 disables it, so the tile kernel runs everywhere.
@@ -333,8 +360,12 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
         (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
         (rc = upload(&w->d_values, values, nvalues)) ||
-        (rc = upload(&w->d_stream, reinterpret_cast<const uint4*>(stream.data()), stream.size() / 16)) ||
-        (rc = upload(&w->d_bin_beg, bin_beg.data(), bin_beg.size()))) {
+        (rc = upload(&w->d_stream, reinterpret_cast<const uint4*>(bs.stream.data()), bs.stream.size() / 16)) ||
+        (rc = upload(&w->d_bin_beg, bs.bin_beg.data(), bs.bin_beg.size())) ||
+        (steps_fast != steps_strict &&
+         ((rc = upload(&w->d_stream_fast, reinterpret_cast<const uint4*>(bf.stream.data()),
+                       bf.stream.size() / 16)) ||
+          (rc = upload(&w->d_bin_beg_fast, bf.bin_beg.data(), bf.bin_beg.size()))))) {
         free_weights(w);
         return rc;
     }
@@ -463,8 +494,10 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.act = act;
     a.out = out;
     a.bias = bias;
-    a.stream = w->d_stream;
-    a.bin_beg = w->d_bin_beg;
+    const bool fast_stream = mode == SPCV_MODE_FAST && w->d_stream_fast != nullptr;
+    a.stream = fast_stream ? w->d_stream_fast : w->d_stream;
+    a.bin_beg = fast_stream ? w->d_bin_beg_fast : w->d_bin_beg;
+    a.steps = mode == SPCV_MODE_FAST ? w->STEPS_fast : w->STEPS;
     a.N = N;
     a.K = w->cols;
     a.M = w->rows;

@@ -59,7 +59,8 @@ struct spcv_cu_weights {
     int LPR = 32;        // lanes per block row
     int NF = 4;          // float4 column quads per lane
     int T = 128;         // virtual columns per tile (LPR * NF * 4)
-    int STEPS = 4;       // steps per chunk of the weight stream (2 or 4)
+    int STEPS = 4;       // steps per chunk of the weight stream (2 or 4), strict mode
+    int STEPS_fast = 4;  // fast mode (a second stream is packed when it differs)
     int device = 0;
     size_t nblocks = 0;
     size_t nchunks = 0;
@@ -70,6 +71,8 @@ struct spcv_cu_weights {
     // execution schedule
     uint4* d_stream = nullptr;
     uint32_t* d_bin_beg = nullptr;
+    uint4* d_stream_fast = nullptr;     // null: fast mode shares the strict stream
+    uint32_t* d_bin_beg_fast = nullptr;
     // small-K path (jit.cu): host copy of the matrix and the compiled variants
     bool jit_eligible = false;
     std::vector<uint32_t> h_row_ptr, h_col_idx;

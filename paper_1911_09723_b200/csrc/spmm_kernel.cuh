@@ -66,6 +66,7 @@ struct KernelArgs {
     // the last, partial wave of tiles still covers every SM.
     long long tail_start;
     int tail_split;
+    int steps;               // steps per chunk of `stream` (host-side dispatch)
     // {1.0f, 1.0f} as f32x2, passed at run time so ptxas cannot fold the
     // strict pair mul.rn.f32x2 + fma.rn.f32x2(acc, one, p) into one FFMA2.
     unsigned long long one2;
