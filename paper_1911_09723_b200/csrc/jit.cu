@@ -480,8 +480,13 @@ int jit_compile(const std::string& src, std::vector<char>& cubin) {
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), "spcv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
         return fail(SPCV_ERR_UNSUPPORTED, "jit: nvrtcCreateProgram failed");
-    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false"};
-    if (nvrtcCompileProgram(prog, 3, opts) != NVRTC_SUCCESS) {
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false"};
+    static const std::string maxrreg = [] {
+        const char* e = std::getenv("SPCV_JIT_MAXRREG");  // tuning knob (occupancy experiments)
+        return e ? std::string("--maxrregcount=") + e : std::string();
+    }();
+    if (!maxrreg.empty()) opts.push_back(maxrreg.c_str());
+    if (nvrtcCompileProgram(prog, static_cast<int>(opts.size()), opts.data()) != NVRTC_SUCCESS) {
         size_t n = 0;
         nvrtcGetProgramLogSize(prog, &n);
         std::string log(n, '\0');

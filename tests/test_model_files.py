@@ -192,3 +192,27 @@ def test_fused_depthwise_pointwise_matches_unfused(ref, files, monkeypatch, name
     assert np.array_equal(outs["1"].view(np.uint32), want.view(np.uint32))
     assert np.array_equal(outs["0"].view(np.uint32), want.view(np.uint32))
     assert launches["1"] < launches["0"], launches
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_random_mbv1_files_forward_bit_exact(ref, seed):
+    """Python-written MBv1 files with seeded random width / sparsity / input size
+    / block plan: spcv_cu_model_forward equals the reference run_network."""
+    import torch
+
+    from paper_1911_09723_b200 import netfile
+
+    rng = np.random.default_rng(seed)
+    width = float(rng.choice([0.25, 0.5]))
+    sparsity = float(rng.choice([0.5, 0.8, 0.95]))
+    hw = int(rng.choice([32, 64, 96]))
+    net = netfile.build_mbv1(width, sparsity, seed=seed, input_hw=hw, num_classes=int(rng.integers(10, 100)),
+                             block_start=int(rng.integers(1, 14)), block_h_after=int(rng.choice([1, 2, 4])))
+    data = netfile.serialize(net)
+    assert ref.model_parse(data)[0] == 0
+    x = rng.uniform(-1, 1, (2, hw, hw, 3)).astype(np.float32)
+    want = ref.run_model(data, x)
+    m = sp.DeviceModel(data)
+    got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
