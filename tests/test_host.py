@@ -47,6 +47,9 @@ def test_cabi_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
+CAP = 1 << 20
+
+
 def _jit_compile(m, mode, act_kind=1, has_bias=1, has_res=0, m_out=None):
     lib = ctypes.CDLL(os.path.join(LIBDIR, "libspcv_cu.so"))
     fn = lib.spcvx_jit_compile
@@ -57,11 +60,11 @@ def _jit_compile(m, mode, act_kind=1, has_bias=1, has_res=0, m_out=None):
     ci = np.ascontiguousarray(m.col_idx, np.uint32)
     va = np.ascontiguousarray(m.values, np.float32)
     sb, cb, nseg = Z(), Z(), I()
-    buf = ctypes.create_string_buffer(1 << 20)
+    buf = ctypes.create_string_buffer(CAP)
     rc = fn(m.rows, m.cols, m.block_h, rp.ctypes.data, ci.ctypes.data if ci.size else None, ci.size,
             va.ctypes.data if va.size else None, mode, act_kind, has_bias, has_res,
             m.rows if m_out is None else m_out, 148, ctypes.byref(nseg), ctypes.byref(sb),
-            ctypes.byref(cb), buf, 1 << 20)
+            ctypes.byref(cb), buf, CAP)
     return rc, buf.value.decode(), cb.value, nseg.value
 
 

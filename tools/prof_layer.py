@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
+    ap.add_argument("--check", type=int, default=0,
+                    help="compare the first N images with the CPU oracle (strict: bit-exact)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     layers = {L.name: (i, L) for i, L in enumerate(cfg["layers"]())}
@@ -59,6 +61,18 @@ def run_layer(args, cfg, li, L, name):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     us = statistics.median(ts)
+    if args.check:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Oracle  # checker only
+        import numpy as np
+        n = args.check
+        got = o[:n].cpu().numpy()
+        want = Oracle().spmm(d.weights, d.act[:n], d.bias, L.act, nthreads=os.cpu_count() or 1).reshape(got.shape)
+        if args.mode == "strict":
+            bad = int((got.view(np.uint32) != want.view(np.uint32)).sum())
+        else:
+            bad = int((np.abs(got - want) > 1e-4 * (1 + np.abs(want))).sum())
+        print(f"{name} check {n} images: {'OK' if bad == 0 else f'{bad} MISMATCHES'}")
     print(f"{name} kernel={kern} (prep {prep:.1f}s) K={L.cin} M={L.cout} S={L.spatial} images={images} slots={dw.row_slots} "
           f"median {us:.1f} us  {d.flops() / us / 1e3:.0f} GFLOP/s  {d.alg_bytes() / us / 1e3:.0f} GB/s "
           f"(alg bytes {d.alg_bytes():.0f})")
