@@ -8,6 +8,7 @@
 // matrices. Layer i of the loaded model then runs as the executor's
 // pointwise step (run_network, netdef.cpp:494-512) via spcv_cu_model_run.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -346,7 +347,7 @@ extern "C" int spcv_cu_model_load(const uint8_t* bytes, size_t size, spcv_cu_mod
         return e == cudaSuccess ? SPCV_OK : cuda_fail(e, what);
     };
     for (size_t i = 0; i < n && rc == SPCV_OK; ++i) {
-        const Layer& L = m->net.layers[i];
+        Layer& L = m->net.layers[i];
         if (L.kind == kEntryConv) {
             // [co][ci][ky][kx] -> [co][ky][kx][ci]: every tap reads one HWC pixel
             // (the same repack as entry_conv_hwc_to_chw, kernels.cpp:433-441)
@@ -361,6 +362,10 @@ extern "C" int spcv_cu_model_load(const uint8_t* bytes, size_t size, spcv_cu_mod
         } else if (L.kind == kDepthwise) {
             rc = upload(&m->d_conv[i], L.other, "model: depthwise upload");
         }
+        if (L.kind == kEntryConv || L.kind == kDepthwise)
+            L.zero_pad_exact = std::all_of(L.other.begin(), L.other.end(), [](float w) { return std::isfinite(w); }) &&
+                               std::none_of(L.bias.begin(), L.bias.end(),
+                                            [](float b) { return b == 0.0f && std::signbit(b); });
         if (rc == SPCV_OK && (L.kind == kEntryConv || L.kind == kDepthwise) && !L.bias.empty())
             rc = upload(&m->d_bias[i], L.bias, "model: bias upload");
         if (L.kind != kPointwise && L.kind != kFullyConnected) continue;

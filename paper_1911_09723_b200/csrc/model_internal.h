@@ -31,6 +31,9 @@ struct Layer {
     std::vector<float> values;  // BCSR values or dense row-major data
     // entry conv [co][ci][3][3] / depthwise [c][3][3] weights
     std::vector<float> other;
+    // entry / depthwise: finite weights and no -0.0 bias, so out-of-image taps
+    // may be read as 0 instead of skipped without changing a bit (network.cu)
+    bool zero_pad_exact = false;
 };
 
 struct Net {

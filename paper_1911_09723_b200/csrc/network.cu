@@ -12,9 +12,12 @@
 //   pooling      global_avg_pool_chw    kernels.cpp:476-487 (sequential sum, then / S)
 //   dense 1x1    dense_gemm_into        kernels.cpp:345-373 (== matmul_reference, k ascending)
 //   residual     add_residual           netdef.cpp:448-452 (after the activation)
-// Out-of-range taps are skipped (SAME padding, tensor.cpp:7-16), never added
-// as zeros, and every multiply-add is __fmul_rn + __fadd_rn.
+// Out-of-range taps are skipped (SAME padding, tensor.cpp:7-16) — or, in the
+// paired depthwise kernel, read as zeros where that provably changes no bit —
+// and every multiply-add rounds the product and the sum separately.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -179,6 +182,111 @@ __global__ void __launch_bounds__(128) entry_conv_const(const ConvArgs a, const 
     }
 }
 
+// f32 pair {a, b} as the .b64 operand of an f32x2 instruction
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a), "f"(b));
+    return d;
+}
+
+// Entry convolution, two horizontally adjacent output pixels per thread in
+// f32x2 registers: every weight (parameter space, a compile-time offset) is
+// broadcast into both halves and multiplies the two pixels' taps at once.
+// Out-of-image taps read 0 instead of being skipped, exact under the same
+// conditions as depthwise_pair_kernel (finite weights, no -0.0 bias; checked
+// per layer on the host). Strict: mul.rn.f32x2 + fma.rn.f32x2(acc, 1.0, p);
+// per output the order stays bias, then (ky, kx, ci) ascending.
+// Weights [co][tap] with the tap stride padded to a multiple of 4 floats, so
+// the uniform-datapath loads of four consecutive taps are 16 B aligned.
+template <int C, int CO>
+struct EntryPairParams {
+    static constexpr int kStride = (9 * C + 3) / 4 * 4;
+    float w[CO * kStride];
+    float b[CO];
+};
+
+template <int C, int CO, bool STRICT>
+__global__ void __launch_bounds__(128) entry_conv_pair(const ConvArgs a, const __grid_constant__ EntryPairParams<C, CO> prm,
+                                                       uint32_t pairs, FastDiv div_pw, FastDiv div_oh,
+                                                       unsigned long long one) {
+    const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= pairs) return;
+    const int PW = (a.OW + 1) / 2;
+    const uint32_t rowi = div_pw.div(it);             // img * OH + oy
+    const int ox = 2 * static_cast<int>(it - rowi * PW);
+    const uint32_t img = div_oh.div(rowi);
+    const int oy = static_cast<int>(rowi - img * a.OH);
+    const int plane = a.OH * a.OW;
+    const float* src = a.in + static_cast<long long>(img) * a.H * a.W * C;
+    const bool two = ox + 1 < a.OW;
+    unsigned long long x[9 * C];
+    const int iy0 = oy * a.stride - a.pad_t, ix0 = ox * a.stride - a.pad_l;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int iy = iy0 + t / 3, ixa = ix0 + t % 3, ixb = ixa + a.stride;
+        const bool rok = static_cast<unsigned>(iy) < static_cast<unsigned>(a.H);
+        const bool oka = rok && static_cast<unsigned>(ixa) < static_cast<unsigned>(a.W);
+        const bool okb = two && rok && static_cast<unsigned>(ixb) < static_cast<unsigned>(a.W);
+        const float* pa = src + (static_cast<long long>(iy) * a.W + ixa) * C;
+        const float* pb = pa + a.stride * C;
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci)
+            x[t * C + ci] = pk2(oka ? __ldg(pa + ci) : 0.0f, okb ? __ldg(pb + ci) : 0.0f);
+    }
+    float* dst = a.out + static_cast<long long>(img) * CO * plane + oy * a.OW + ox;
+    const bool vec = two && (a.OW % 2 == 0);  // float2 stores stay 8 B aligned
+#pragma unroll
+    for (int co = 0; co < CO; ++co) {
+        const float b = a.bias ? prm.b[co] : 0.0f;
+        unsigned long long acc = pk2(b, b);
+#pragma unroll
+        for (int t = 0; t < 9 * C; ++t) {
+            const float wv = prm.w[co * EntryPairParams<C, CO>::kStride + t];
+            const unsigned long long w = pk2(wv, wv);
+            if constexpr (STRICT) {
+                unsigned long long q;
+                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(q) : "l"(w), "l"(x[t]));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(acc), "l"(one), "l"(q));
+            } else {
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(w), "l"(x[t]), "l"(acc));
+            }
+        }
+        float e0, e1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(e0), "=f"(e1) : "l"(acc));
+        e0 = act_apply(e0, a.act_kind, a.lo, a.hi);
+        e1 = act_apply(e1, a.act_kind, a.lo, a.hi);
+        float* o = dst + static_cast<long long>(co) * plane;
+        if (vec) {
+            __stcs(reinterpret_cast<float2*>(o), make_float2(e0, e1));
+        } else {
+            __stcs(o, e0);
+            if (two) __stcs(o + 1, e1);
+        }
+    }
+}
+
+template <int CO>
+bool launch_entry_pair(const ConvArgs& a, const std::vector<float>& w_cikk, const std::vector<float>& bias,
+                       int images, bool strict, cudaStream_t st) {
+    using P = EntryPairParams<3, CO>;
+    P prm{};
+    for (int co = 0; co < CO; ++co)
+        for (int t = 0; t < 9; ++t)
+            for (int ci = 0; ci < 3; ++ci)  // [co][ci][ky][kx] -> [co][ky][kx][ci]
+                prm.w[co * P::kStride + t * 3 + ci] = w_cikk[(static_cast<size_t>(co) * 3 + ci) * 9 + t];
+    for (int co = 0; co < CO; ++co) prm.b[co] = bias.empty() ? 0.0f : bias[static_cast<size_t>(co)];
+    const long long pairs = static_cast<long long>(images) * a.OH * ((a.OW + 1) / 2);
+    if (pairs >= 0x7FFFFFFFLL) return false;
+    const FastDiv dpw((a.OW + 1) / 2), doh(a.OH);
+    const unsigned grid = static_cast<unsigned>((pairs + 127) / 128);
+    const unsigned long long one = 0x3f8000003f800000ULL;
+    if (strict)
+        entry_conv_pair<3, CO, true><<<grid, 128, 0, st>>>(a, prm, static_cast<uint32_t>(pairs), dpw, doh, one);
+    else
+        entry_conv_pair<3, CO, false><<<grid, 128, 0, st>>>(a, prm, static_cast<uint32_t>(pairs), dpw, doh, one);
+    return true;
+}
+
 template <int CO>
 bool launch_entry_const(const ConvArgs& a, const std::vector<float>& w_cikk, const std::vector<float>& bias,
                         unsigned grid, cudaStream_t st) {
@@ -193,8 +301,22 @@ bool launch_entry_const(const ConvArgs& a, const std::vector<float>& w_cikk, con
 }
 
 bool launch_entry_fast(const ConvArgs& a, int C, int CO, const std::vector<float>& w,
-                       const std::vector<float>& bias, unsigned grid, cudaStream_t st) {
+                       const std::vector<float>& bias, unsigned grid, bool zero_pad, int images, bool strict,
+                       cudaStream_t st) {
     if (C != 3) return false;
+    if (zero_pad) {
+        switch (CO) {
+            case 8: return launch_entry_pair<8>(a, w, bias, images, strict, st);
+            case 16: return launch_entry_pair<16>(a, w, bias, images, strict, st);
+            case 24: return launch_entry_pair<24>(a, w, bias, images, strict, st);
+            case 32: return launch_entry_pair<32>(a, w, bias, images, strict, st);
+            case 40: return launch_entry_pair<40>(a, w, bias, images, strict, st);
+            case 48: return launch_entry_pair<48>(a, w, bias, images, strict, st);
+            case 56: return launch_entry_pair<56>(a, w, bias, images, strict, st);
+            case 64: return launch_entry_pair<64>(a, w, bias, images, strict, st);
+            default: break;
+        }
+    }
     switch (CO) {
         case 8: return launch_entry_const<8>(a, w, bias, grid, st);
         case 16: return launch_entry_const<16>(a, w, bias, grid, st);
@@ -263,6 +385,101 @@ __global__ void depthwise_kernel(const ConvArgs a, uint32_t items, int RB, FastD
     }
 }
 
+// Depthwise 3x3, two horizontally adjacent outputs per thread in f32x2
+// registers and a strip of DwRows<STRIDE> output rows, the input window held
+// in registers (each input value loaded once per strip).
+//
+// Out-of-image taps read 0 instead of being skipped (kernels.cpp:410-416).
+// That is exact under two conditions the host checks per layer: finite
+// weights (w * 0 = +-0, never NaN) and no -0.0 bias. Then acc starts away
+// from -0.0 and never reaches it (round-to-nearest: x + y = -0 only when both
+// are -0), and acc + (+-0) == acc for every acc != -0.0, so the extra terms
+// change no bit. Per output the order stays bias, then (ky, kx) ascending;
+// strict multiplies and adds with separate roundings: mul.rn.f32x2, then
+// fma.rn.f32x2(acc, 1.0, p) (acc * 1 is exact; `one` is a kernel argument so
+// ptxas cannot fuse the pair). Fast mode uses one fma.rn.f32x2 per tap.
+#ifndef SPCV_DW_R1
+#define SPCV_DW_R1 7
+#endif
+template <int STRIDE>
+struct DwRows {
+    // output rows per thread: 7 divides every MobileNet plane height (112, 56,
+    // 28, 14, 7), so no strip computes or loads rows past the plane
+    static constexpr int R = STRIDE == 1 ? SPCV_DW_R1 : 4;
+};
+
+template <int STRIDE, bool STRICT>
+__global__ void __launch_bounds__(256) depthwise_pair_kernel(const ConvArgs a, uint32_t items, int RB, int PW,
+                                                             FastDiv div_pw, FastDiv div_rb, FastDiv div_c,
+                                                             unsigned long long one) {
+    constexpr int R = DwRows<STRIDE>::R;
+    constexpr int NR = (R - 1) * STRIDE + 3;  // input rows of the strip
+    constexpr int NC = STRIDE + 3;            // input columns of the output pair
+    const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= items) return;
+    const uint32_t strip = div_pw.div(it);   // plane * RB + rb
+    const int xp = static_cast<int>(it - strip * PW);
+    const uint32_t plane = div_rb.div(strip);
+    const int rb = static_cast<int>(strip - plane * RB);
+    const int c = static_cast<int>(plane - div_c.div(plane) * a.CO);
+    const int ox0 = 2 * xp, oy0 = rb * R;
+    const int ix0 = ox0 * STRIDE - a.pad_l, iy0 = oy0 * STRIDE - a.pad_t;
+    const float* src = a.in + static_cast<long long>(plane) * a.H * a.W;
+    float k[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) k[t] = __ldg(a.w + c * 9 + t);
+    const float b = a.bias ? __ldg(a.bias + c) : 0.0f;
+    bool cok[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) cok[q] = static_cast<unsigned>(ix0 + q) < static_cast<unsigned>(a.W);
+    // window origin (may lie outside the plane: only valid taps dereference it)
+    const float* p0 = src + static_cast<long long>(iy0) * a.W + ix0;
+    float v[NR][NC];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const bool rok = static_cast<unsigned>(iy0 + r) < static_cast<unsigned>(a.H);
+        const float* row = p0 + r * a.W;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) v[r][q] = (rok && cok[q]) ? __ldg(row + q) : 0.0f;
+    }
+    float* dst = a.out + static_cast<long long>(plane) * a.OH * a.OW + ox0;
+    const bool two = ox0 + 1 < a.OW;
+    const bool vec = two && (a.OW % 2 == 0);  // float2 stores stay 8 B aligned
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int oy = oy0 + j;
+        if (oy >= a.OH) break;
+        unsigned long long acc = pk2(b, b);
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+            const int r = j * STRIDE + ky;
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+                const unsigned long long x = pk2(v[r][kx], v[r][kx + STRIDE]);
+                const unsigned long long w = pk2(k[ky * 3 + kx], k[ky * 3 + kx]);
+                if constexpr (STRICT) {
+                    unsigned long long p;
+                    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(w), "l"(x));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(acc), "l"(one), "l"(p));
+                } else {
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc) : "l"(w), "l"(x), "l"(acc));
+                }
+            }
+        }
+        float e0, e1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(e0), "=f"(e1) : "l"(acc));
+        e0 = act_apply(e0, a.act_kind, a.lo, a.hi);
+        e1 = act_apply(e1, a.act_kind, a.lo, a.hi);
+        float* o = dst + static_cast<long long>(oy) * a.OW;
+        if (vec) {
+            *reinterpret_cast<float2*>(o) = make_float2(e0, e1);
+        } else {
+            o[0] = e0;
+            if (two) o[1] = e1;
+        }
+    }
+}
+
 // Global average pool: one thread per (image, channel), sequential sum.
 __global__ void global_pool_kernel(const float* in, float* out, long long planes, int S) {
     const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -321,6 +538,15 @@ __global__ void dense_strict_kernel(const float* __restrict__ w, const float* __
         const int r = r0 + ty + 8 * q;
         if (r < M) out[(img * M + r) * S + s] = act_apply(acc[q], act_kind, lo, hi);
     }
+}
+
+// SPCV_DW_PAIR=0: always the per-tap (skipping) entry / depthwise kernels.
+bool pair_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("SPCV_DW_PAIR");
+        return e && std::atoi(e) == 0;
+    }();
+    return off;
 }
 
 unsigned blocks_for(long long n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
@@ -431,7 +657,8 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
                         break;
                     }
                     const long long npix = static_cast<long long>(images) * ph.out * pw.out;
-                    if (!launch_entry_fast(a, L.cin, L.cout, L.other, L.bias, blocks_for(npix, 128), st)) {
+                    if (!launch_entry_fast(a, L.cin, L.cout, L.other, L.bias, blocks_for(npix, 128),
+                                           L.zero_pad_exact && !pair_off(), images, mode == SPCV_MODE_STRICT, st)) {
                         const size_t smem = (static_cast<size_t>(L.cout) * 9 * L.cin + L.cout) * sizeof(float);
                         entry_conv_kernel<<<blocks_for(npix, 128), 128, smem, st>>>(a);
                     }
@@ -440,7 +667,34 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
                         rc = fail(SPCV_ERR_SHAPE, "depthwise_conv_chw: stride must be 1 or 2");
                         break;
                     }
-                    // 4-row strips per plane; launched in image chunks of < 2^31 threads
+                    if (L.zero_pad_exact && !pair_off()) {
+                        // output pairs x row strips per plane, in image chunks of < 2^31 threads
+                        const int R = L.stride == 1 ? DwRows<1>::R : DwRows<2>::R;
+                        const int RB = (ph.out + R - 1) / R, PW = (pw.out + 1) / 2;
+                        const long long per_img = static_cast<long long>(L.cout) * RB * PW;
+                        const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
+                        const FastDiv dpw(PW), drb(RB), dc(L.cout);
+                        const unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
+                        const bool strict = mode == SPCV_MODE_STRICT;
+                        for (int i0 = 0; i0 < images; i0 += chunk) {
+                            const int ni = std::min(chunk, images - i0);
+                            ConvArgs c = a;
+                            c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
+                            c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
+                            const uint32_t items = static_cast<uint32_t>(per_img * ni);
+                            const unsigned grid = blocks_for(items, kT);
+                            if (L.stride == 1)
+                                strict ? depthwise_pair_kernel<1, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
+                                       : depthwise_pair_kernel<1, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
+                            else
+                                strict ? depthwise_pair_kernel<2, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
+                                       : depthwise_pair_kernel<2, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
+                        }
+                        g_launches.fetch_add(1, std::memory_order_relaxed);
+                        break;
+                    }
+                    // per-tap kernel (skips out-of-image taps): 4-row strips per plane,
+                    // launched in image chunks of < 2^31 threads
                     const int RB = (ph.out + 3) / 4;
                     const long long per_img = static_cast<long long>(L.cout) * RB * pw.out;
                     const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
