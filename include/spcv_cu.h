@@ -176,10 +176,14 @@ int spcv_cu_model_layer(const spcv_cu_model* m, int i, int* info);
 /* Borrowed packed weights of sparse layer i (owned by the model). */
 int spcv_cu_model_weights(const spcv_cu_model* m, int i, const spcv_cu_weights** w);
 
-/* Run 1x1 / classifier layer i as run_network's pointwise step
- * (netdef.cpp:494-512): its bias, fused activation, padded-row truncation,
- * and the residual (device [images][cout][out_h*out_w], required iff the
- * layer has a residual source). act [images][cin][in_h*in_w] on device. */
+/* Run layer i of the executor on device tensors. A 1x1 / classifier layer
+ * runs as run_network's pointwise step (netdef.cpp:494-512): its bias, fused
+ * activation, padded-row truncation, and the residual (device
+ * [images][cout][out_h*out_w], required iff the layer has a residual source).
+ * An entry convolution (act: HWC images), depthwise 3x3 (depthwise_conv_chw,
+ * kernels.cpp:385-422) or global-pool layer runs as in
+ * spcv_cu_model_forward (residual ignored). act [images][cin][in_h*in_w]
+ * (CHW) on device; out [images][cout][out_h*out_w]. */
 int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act, int images,
                       const float* residual, float* out, int mode, void* stream);
 
@@ -190,8 +194,8 @@ int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act, int image
  * sparse 1x1 / classifier layers (spcv_cu_spmm_layer) run as CUDA kernels, in
  * stream order on `stream`, with a stream-ordered workspace. In
  * SPCV_MODE_STRICT the logits are bit-identical to the reference's
- * run_network; SPCV_MODE_FAST uses FFMA in the SpMM and cuBLAS for dense
- * 1x1 layers. Input dims other than the model's -> SPCV_ERR_SHAPE
+ * run_network; SPCV_MODE_FAST uses fused multiply-adds (SpMM, entry and
+ * depthwise convolutions) and cuBLAS for dense 1x1 layers. Input dims other than the model's -> SPCV_ERR_SHAPE
  * (check_run_inputs, netdef.cpp:433-441). */
 int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images, int in_h,
                           int in_w, int in_c, float* logits, int mode, void* stream);

@@ -141,6 +141,10 @@ class Ref:
         lib.ref_run_model.argtypes = [_p, _z, _p, _i, _i, _p, ctypes.POINTER(_i)]
         lib.ref_model_layer.argtypes = [_p, _z, _i, _p, _p, _p, _p, _p]
         lib.ref_bench_layers.argtypes = [ctypes.POINTER(RefLayer), _i, _i, _i, _i, ctypes.POINTER(_d)]
+        lib.ref_depthwise.argtypes = [_i, _i, _i, _i, _i, _p, _p, _i, _f, _f, _p, _p, ctypes.POINTER(_i),
+                                      ctypes.POINTER(_i)]
+        lib.ref_entry_conv.argtypes = [_i, _i, _i, _i, _i, _i, _p, _p, _i, _f, _f, _p, _p, ctypes.POINTER(_i),
+                                       ctypes.POINTER(_i)]
         lib.ref_bench_spmm.argtypes = [_i, _i, _i, _p, _z, _p, _z, _p, _z, _i, _i, _i, _p, _p, _i,
                                        _f, _f, _p, _i, _i, _i, ctypes.POINTER(_d)]
         self.lib = lib
@@ -243,6 +247,37 @@ class Ref:
                                     1 if reference_executor else 0, out.ctypes.data, ctypes.byref(classes))
         if rc:
             raise RuntimeError(f"ref_run_model: code {rc}")
+        return out
+
+    def depthwise(self, x, w, bias, stride, act_kind=0, lo=0.0, hi=0.0):
+        """spcv::depthwise_conv_chw per image: x [B][C][H][W], w [C][3][3] -> [B][C][OH][OW]."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = np.ascontiguousarray(w, np.float32)
+        b = None if bias is None else np.ascontiguousarray(bias, np.float32)
+        B, C, H, W = x.shape
+        oh, ow = (H + stride - 1) // stride, (W + stride - 1) // stride  # same_pad out
+        out = np.zeros((B, C, oh, ow), np.float32)
+        r_oh, r_ow = _i(), _i()
+        rc = self.lib.ref_depthwise(B, C, H, W, stride, w.ctypes.data, None if b is None else b.ctypes.data,
+                                    act_kind, lo, hi, x.ctypes.data, out.ctypes.data, ctypes.byref(r_oh),
+                                    ctypes.byref(r_ow))
+        assert rc == 0 and (B == 0 or (r_oh.value, r_ow.value) == (oh, ow)), rc
+        return out
+
+    def entry_conv(self, x_hwc, w, bias, stride, act_kind=0, lo=0.0, hi=0.0):
+        """spcv::entry_conv_hwc_to_chw per image: x [B][H][W][C], w [CO][C][3][3] -> [B][CO][OH][OW]."""
+        x = np.ascontiguousarray(x_hwc, np.float32)
+        w = np.ascontiguousarray(w, np.float32)
+        b = None if bias is None else np.ascontiguousarray(bias, np.float32)
+        B, H, W, C = x.shape
+        CO = w.shape[0]
+        oh, ow = (H + stride - 1) // stride, (W + stride - 1) // stride  # same_pad out
+        out = np.zeros((B, CO, oh, ow), np.float32)
+        r_oh, r_ow = _i(), _i()
+        rc = self.lib.ref_entry_conv(B, C, H, W, CO, stride, w.ctypes.data, None if b is None else b.ctypes.data,
+                                     act_kind, lo, hi, x.ctypes.data, out.ctypes.data, ctypes.byref(r_oh),
+                                     ctypes.byref(r_ow))
+        assert rc == 0 and (B == 0 or (r_oh.value, r_ow.value) == (oh, ow)), rc
         return out
 
     def model_parse(self, data: bytes):

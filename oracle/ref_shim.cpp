@@ -131,6 +131,54 @@ int ref_matmul_reference(int rows, int cols, int H, int W, const float* w, const
     }
 }
 
+// spcv::depthwise_conv_chw (kernels.cpp:385-422) per image: in [images][C][H][W],
+// w [C][3][3], bias [C] or null -> out [images][C][OH][OW].
+int ref_depthwise(int images, int C, int H, int W, int stride, const float* w, const float* bias,
+                  int act_kind, float lo, float hi, const float* in, float* out, int* OH, int* OW) {
+    try {
+        spcv::DepthwiseWeights dw(C);
+        std::memcpy(dw.data.data(), w, sizeof(float) * dw.data.size());
+        std::span<const float> b(bias, bias ? static_cast<std::size_t>(C) : 0);
+        const std::size_t in_sz = static_cast<std::size_t>(C) * H * W;
+        std::size_t out_sz = 0;
+        for (int i = 0; i < images; ++i) {
+            spcv::Tensor a(C, H, W, spcv::Layout::CHW);
+            std::memcpy(a.data.data(), in + i * in_sz, in_sz * sizeof(float));
+            const spcv::Tensor o = spcv::depthwise_conv_chw(a, dw, stride, b, make_act(act_kind, lo, hi));
+            out_sz = o.data.size();
+            *OH = o.height;
+            *OW = o.width;
+            if (out) std::memcpy(out + i * out_sz, o.data.data(), out_sz * sizeof(float));
+        }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// spcv::entry_conv_hwc_to_chw (kernels.cpp:424-474) per image: in [images][H][W][C]
+// (HWC), w [CO][C][3][3], bias [CO] or null -> out [images][CO][OH][OW].
+int ref_entry_conv(int images, int C, int H, int W, int CO, int stride, const float* w, const float* bias,
+                   int act_kind, float lo, float hi, const float* in, float* out, int* OH, int* OW) {
+    try {
+        spcv::ConvWeights cw(CO, C, 3, 3);
+        std::memcpy(cw.data.data(), w, sizeof(float) * cw.data.size());
+        std::span<const float> b(bias, bias ? static_cast<std::size_t>(CO) : 0);
+        const std::size_t in_sz = static_cast<std::size_t>(C) * H * W;
+        for (int i = 0; i < images; ++i) {
+            spcv::Tensor a(C, H, W, spcv::Layout::HWC);
+            std::memcpy(a.data.data(), in + i * in_sz, in_sz * sizeof(float));
+            const spcv::Tensor o = spcv::entry_conv_hwc_to_chw(a, cw, stride, b, make_act(act_kind, lo, hi));
+            *OH = o.height;
+            *OW = o.width;
+            if (out) std::memcpy(out + i * o.data.size(), o.data.data(), o.data.size() * sizeof(float));
+        }
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
 int ref_encode_bcsr(int rows, int cols, int block_h, const float* w, std::uint32_t* row_ptr,
                     std::uint32_t* col_idx, float* values, std::size_t* nblocks) {
     try {

@@ -429,6 +429,14 @@ extern "C" int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act
         return fail(SPCV_ERR_INVALID, "model: layer index out of range");
     const size_t k = static_cast<size_t>(i);
     const Layer& L = m->net.layers[k];
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "model: unknown arithmetic mode");
+    if (L.kind == kEntryConv || L.kind == kDepthwise || L.kind == kGlobalPool) {
+        if (images < 0) return fail(SPCV_ERR_SHAPE, "model: negative image count");
+        if (images == 0) return SPCV_OK;
+        if (!act || !out) return fail(SPCV_ERR_INVALID, "model: null tensor pointer");
+        return run_spatial_layer(m, k, act, images, out, mode, static_cast<cudaStream_t>(stream));
+    }
     if (L.kind != kPointwise && L.kind != kFullyConnected)
         return fail(SPCV_ERR_INVALID, "model: layer " + L.name + " is not a 1x1 / classifier layer");
     if (L.residual_src >= 0 && !residual)

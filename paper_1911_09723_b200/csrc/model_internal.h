@@ -46,6 +46,14 @@ struct Net {
 
 }  // namespace spcv_model
 
+struct spcv_cu_model;
+namespace spcv_model {
+// network.cu: one entry-convolution, depthwise or global-pool layer on device
+// tensors (SPCV_ERR_INVALID for other kinds).
+int run_spatial_layer(const spcv_cu_model* m, size_t i, const float* in, int images, float* out, int mode,
+                      cudaStream_t st);
+}  // namespace spcv_model
+
 struct spcv_cu_model {
     spcv_model::Net net;
     int device = 0;

@@ -553,6 +553,87 @@ unsigned blocks_for(long long n, int t) { return static_cast<unsigned>((n + t - 
 
 }  // namespace
 
+namespace spcv_model {
+
+// One entry-convolution, depthwise or global-pool layer of the executor on
+// device tensors (in: the layer's input for `images` images, out: its output).
+int run_spatial_layer(const spcv_cu_model* m, size_t i, const float* in, int images, float* out, int mode,
+                      cudaStream_t st) {
+    constexpr int kT = 256;
+    const Layer& L = m->net.layers[i];
+    const long long out_elems = static_cast<long long>(images) * L.cout * L.out_h * L.out_w;
+    if (L.kind == kGlobalPool) {
+        const long long planes = static_cast<long long>(images) * L.cin;
+        global_pool_kernel<<<blocks_for(planes, kT), kT, 0, st>>>(in, out, planes, L.in_h * L.in_w);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return SPCV_OK;
+    }
+    if (L.kind != kEntryConv && L.kind != kDepthwise)
+        return fail(SPCV_ERR_INVALID, "model: layer " + L.name + " is not a spatial layer");
+    const Pad ph = same_pad(L.in_h, 3, L.stride), pw = same_pad(L.in_w, 3, L.stride);
+    ConvArgs a{in, m->d_conv[i], m->d_bias[i], out, out_elems, L.in_h, L.in_w, L.cin, L.cout,
+               ph.out, pw.out, L.stride, ph.before, pw.before, L.act_kind, L.lo, L.hi};
+    const bool strict = mode == SPCV_MODE_STRICT;
+    if (L.kind == kEntryConv) {
+        if (L.cin > kMaxEntryC)
+            return fail(SPCV_ERR_UNSUPPORTED, "model: entry convolution with more than 4 input channels");
+        const long long npix = static_cast<long long>(images) * ph.out * pw.out;
+        if (!launch_entry_fast(a, L.cin, L.cout, L.other, L.bias, blocks_for(npix, 128),
+                               L.zero_pad_exact && !pair_off(), images, strict, st)) {
+            const size_t smem = (static_cast<size_t>(L.cout) * 9 * L.cin + L.cout) * sizeof(float);
+            entry_conv_kernel<<<blocks_for(npix, 128), 128, smem, st>>>(a);
+        }
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return SPCV_OK;
+    }
+    if (L.stride != 1 && L.stride != 2) return fail(SPCV_ERR_SHAPE, "depthwise_conv_chw: stride must be 1 or 2");
+    if (L.zero_pad_exact && !pair_off()) {
+        // output pairs x row strips per plane, in image chunks of < 2^31 threads
+        const int R = L.stride == 1 ? DwRows<1>::R : DwRows<2>::R;
+        const int RB = (ph.out + R - 1) / R, PW = (pw.out + 1) / 2;
+        const long long per_img = static_cast<long long>(L.cout) * RB * PW;
+        const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
+        const FastDiv dpw(PW), drb(RB), dc(L.cout);
+        const unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
+        for (int i0 = 0; i0 < images; i0 += chunk) {
+            const int ni = std::min(chunk, images - i0);
+            ConvArgs c = a;
+            c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
+            c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
+            const uint32_t items = static_cast<uint32_t>(per_img * ni);
+            const unsigned grid = blocks_for(items, kT);
+            if (L.stride == 1)
+                strict ? depthwise_pair_kernel<1, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
+                       : depthwise_pair_kernel<1, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
+            else
+                strict ? depthwise_pair_kernel<2, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
+                       : depthwise_pair_kernel<2, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
+        }
+    } else {
+        // per-tap kernel (skips out-of-image taps): 4-row strips per plane,
+        // launched in image chunks of < 2^31 threads
+        const int RB = (ph.out + 3) / 4;
+        const long long per_img = static_cast<long long>(L.cout) * RB * pw.out;
+        const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
+        const FastDiv dow(pw.out), drb(RB), dc(L.cout);
+        for (int i0 = 0; i0 < images; i0 += chunk) {
+            const int ni = std::min(chunk, images - i0);
+            ConvArgs c = a;
+            c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
+            c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
+            const uint32_t items = static_cast<uint32_t>(per_img * ni);
+            if (L.stride == 1)
+                depthwise_kernel<1><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
+            else
+                depthwise_kernel<2><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
+        }
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SPCV_OK;
+}
+
+}  // namespace spcv_model
+
 extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images,
                                      int in_h, int in_w, int in_c, float* logits, int mode,
                                      void* stream) {
@@ -647,79 +728,10 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
         bool res_done = false;
         switch (L.kind) {
             case kEntryConv:
-            case kDepthwise: {
-                const Pad ph = same_pad(L.in_h, 3, L.stride), pw = same_pad(L.in_w, 3, L.stride);
-                ConvArgs a{cur, m->d_conv[i], m->d_bias[i], dst, out_elems, L.in_h, L.in_w, L.cin, L.cout,
-                           ph.out, pw.out, L.stride, ph.before, pw.before, L.act_kind, L.lo, L.hi};
-                if (L.kind == kEntryConv) {
-                    if (L.cin > kMaxEntryC) {
-                        rc = fail(SPCV_ERR_UNSUPPORTED, "model: entry convolution with more than 4 input channels");
-                        break;
-                    }
-                    const long long npix = static_cast<long long>(images) * ph.out * pw.out;
-                    if (!launch_entry_fast(a, L.cin, L.cout, L.other, L.bias, blocks_for(npix, 128),
-                                           L.zero_pad_exact && !pair_off(), images, mode == SPCV_MODE_STRICT, st)) {
-                        const size_t smem = (static_cast<size_t>(L.cout) * 9 * L.cin + L.cout) * sizeof(float);
-                        entry_conv_kernel<<<blocks_for(npix, 128), 128, smem, st>>>(a);
-                    }
-                } else {
-                    if (L.stride != 1 && L.stride != 2) {
-                        rc = fail(SPCV_ERR_SHAPE, "depthwise_conv_chw: stride must be 1 or 2");
-                        break;
-                    }
-                    if (L.zero_pad_exact && !pair_off()) {
-                        // output pairs x row strips per plane, in image chunks of < 2^31 threads
-                        const int R = L.stride == 1 ? DwRows<1>::R : DwRows<2>::R;
-                        const int RB = (ph.out + R - 1) / R, PW = (pw.out + 1) / 2;
-                        const long long per_img = static_cast<long long>(L.cout) * RB * PW;
-                        const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
-                        const FastDiv dpw(PW), drb(RB), dc(L.cout);
-                        const unsigned long long one = 0x3f8000003f800000ULL;  // {1.0f, 1.0f}
-                        const bool strict = mode == SPCV_MODE_STRICT;
-                        for (int i0 = 0; i0 < images; i0 += chunk) {
-                            const int ni = std::min(chunk, images - i0);
-                            ConvArgs c = a;
-                            c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
-                            c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
-                            const uint32_t items = static_cast<uint32_t>(per_img * ni);
-                            const unsigned grid = blocks_for(items, kT);
-                            if (L.stride == 1)
-                                strict ? depthwise_pair_kernel<1, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
-                                       : depthwise_pair_kernel<1, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
-                            else
-                                strict ? depthwise_pair_kernel<2, true><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one)
-                                       : depthwise_pair_kernel<2, false><<<grid, kT, 0, st>>>(c, items, RB, PW, dpw, drb, dc, one);
-                        }
-                        g_launches.fetch_add(1, std::memory_order_relaxed);
-                        break;
-                    }
-                    // per-tap kernel (skips out-of-image taps): 4-row strips per plane,
-                    // launched in image chunks of < 2^31 threads
-                    const int RB = (ph.out + 3) / 4;
-                    const long long per_img = static_cast<long long>(L.cout) * RB * pw.out;
-                    const int chunk = static_cast<int>(std::max<long long>(1, 0x7FFFFFFFLL / per_img));
-                    const FastDiv dow(pw.out), drb(RB), dc(L.cout);
-                    for (int i0 = 0; i0 < images; i0 += chunk) {
-                        const int ni = std::min(chunk, images - i0);
-                        ConvArgs c = a;
-                        c.in = a.in + static_cast<long long>(i0) * L.cin * L.in_h * L.in_w;
-                        c.out = a.out + static_cast<long long>(i0) * L.cout * ph.out * pw.out;
-                        const uint32_t items = static_cast<uint32_t>(per_img * ni);
-                        if (L.stride == 1)
-                            depthwise_kernel<1><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
-                        else
-                            depthwise_kernel<2><<<blocks_for(items, kT), kT, 0, st>>>(c, items, RB, dow, drb, dc);
-                    }
-                }
-                g_launches.fetch_add(1, std::memory_order_relaxed);
+            case kDepthwise:
+            case kGlobalPool:
+                rc = spcv_model::run_spatial_layer(m, i, cur, images, dst, mode, st);
                 break;
-            }
-            case kGlobalPool: {
-                const long long planes = static_cast<long long>(images) * L.cin;
-                global_pool_kernel<<<blocks_for(planes, kT), kT, 0, st>>>(cur, dst, planes, L.in_h * L.in_w);
-                g_launches.fetch_add(1, std::memory_order_relaxed);
-                break;
-            }
             case kPointwise:
             case kFullyConnected: {
                 if (m->w[i]) {

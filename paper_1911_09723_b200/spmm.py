@@ -614,7 +614,9 @@ class DeviceModel:
         return w
 
     def run(self, i: int, act, out, residual=None, strict: bool = True, stream=None) -> None:
-        """Layer i as run_network's pointwise step on torch CUDA tensors."""
+        """Layer i on torch CUDA tensors: a 1x1 / classifier layer as run_network's
+        pointwise step; an entry conv (HWC input), depthwise or pool layer as
+        in forward()."""
         import torch
 
         B = act.shape[0]

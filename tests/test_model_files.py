@@ -216,3 +216,109 @@ def test_random_mbv1_files_forward_bit_exact(ref, seed):
     m = sp.DeviceModel(data)
     got = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+# --------------------------- entry conv and depthwise layers vs the reference
+def _spatial_case(seed, input_hw, width=0.25):
+    from paper_1911_09723_b200 import netfile
+
+    net = netfile.build_mbv1(width, 0.9, seed=seed, input_hw=input_hw, num_classes=10)
+    return net
+
+
+def _run_layer(net, i, x, strict=True):
+    import torch
+
+    from paper_1911_09723_b200 import netfile
+
+    m = sp.DeviceModel(netfile.serialize(net))
+    L = m.layers[i]
+    out = torch.empty((x.shape[0], L["cout"], L["out_h"], L["out_w"]), device="cuda")
+    m.run(i, torch.from_numpy(np.ascontiguousarray(x)).cuda(), out, strict=strict)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _ref_layer(ref, net, i, x):
+    L = net.layers[i]
+    kind = 1 if L.act[0] == "clamp" else 0
+    b = L.bias if L.bias.size else None
+    if i == 0:
+        return ref.entry_conv(x, L.weights, b, L.stride, kind, L.act[1], L.act[2])
+    return ref.depthwise(x, L.weights, b, L.stride, kind, L.act[1], L.act[2])
+
+
+def _same_bits(got, want):
+    nan = np.isnan(want)
+    return np.array_equal(np.isnan(got), nan) and np.array_equal(got[~nan].view(np.uint32),
+                                                                 want[~nan].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("input_hw", [64, 33, 18])
+def test_entry_and_depthwise_layers_bit_exact(ref, input_hw):
+    """The executor's entry convolution and every depthwise layer (stride 1
+    and 2, even and odd planes down to 1x1) through spcv_cu_model_run equal
+    the reference's entry_conv_hwc_to_chw / depthwise_conv_chw bit for bit;
+    the inputs include exact +0.0 / -0.0 values. Fast mode stays close."""
+    net = _spatial_case(7, input_hw)
+    rng = np.random.default_rng(input_hw)
+    L0 = net.layers[0]
+    x = rng.uniform(-1, 1, (3, L0.in_h, L0.in_w, L0.cin)).astype(np.float32)
+    x[0, :4] = 0.0
+    x[1, :2] = -0.0
+    for i, L in enumerate(net.layers):
+        if L.kind not in (0, 2):
+            continue
+        if i > 0:  # depthwise input: a CHW activation with zeros of both signs
+            x = rng.uniform(-1, 6, (3, L.cin, L.in_h, L.in_w)).astype(np.float32)
+            x[0] = np.where(x[0] < 1.0, 0.0, x[0])
+            x[1] = np.where(x[1] < 1.0, -0.0, x[1])
+        want = _ref_layer(ref, net, i, x)
+        got = _run_layer(net, i, x)
+        assert _same_bits(got, want), (L.name, float(np.nanmax(np.abs(got - want))))
+        fast = _run_layer(net, i, x, strict=False)
+        assert np.allclose(fast, want, rtol=1e-5, atol=1e-5), L.name
+
+
+@pytest.mark.gpu
+def test_spatial_layers_signed_zero_and_nonfinite_weights(ref):
+    """Adversarial layers for the zero-padded kernels: a -0.0 bias with +0.0
+    inputs and weights whose out-of-image taps are positive (a padded tap
+    would turn the -0.0 result into +0.0), and an infinite weight (0 * inf =
+    NaN at padded taps). Both make the executor fall back to the per-tap
+    kernels, which skip out-of-image taps like the reference: bit-exact (NaN
+    where the reference has NaN)."""
+    net = _spatial_case(9, 16)
+    i_dw = next(i for i, L in enumerate(net.layers) if L.kind == 2 and L.stride == 1)
+    L = net.layers[i_dw]
+    w = -np.abs(L.weights)
+    w[:, 0, :] = 0.5   # top row taps (padded at oy = 0)
+    w[:, :, 0] = 0.5   # left column taps (padded at ox = 0)
+    L.weights = w.astype(np.float32)
+    L.bias = np.full(L.cout, -0.0, np.float32)
+    x = np.zeros((2, L.cin, L.in_h, L.in_w), np.float32)
+    want = _ref_layer(ref, net, i_dw, x)
+    assert np.signbit(want[0, 0, 0, 0]) and want[0, 0, 0, 0] == 0.0  # the reference keeps -0.0
+    assert _same_bits(_run_layer(net, i_dw, x), want)
+    # the same weights with a +0.0 bias take the zero-padded kernel: still exact
+    L.bias = np.zeros(L.cout, np.float32)
+    want = _ref_layer(ref, net, i_dw, x)
+    assert _same_bits(_run_layer(net, i_dw, x), want)
+    # an infinite weight: NaN wherever the reference multiplies it by 0
+    L.weights = w.astype(np.float32)
+    L.weights[0, 2, 2] = np.inf
+    L.bias = (np.random.default_rng(1).standard_normal(L.cout) * 0.1).astype(np.float32)
+    x = np.random.default_rng(2).uniform(0, 6, (2, L.cin, L.in_h, L.in_w)).astype(np.float32)
+    x[:, 0, 3:5, 3:5] = 0.0
+    want = _ref_layer(ref, net, i_dw, x)
+    assert np.isnan(want).any()
+    assert _same_bits(_run_layer(net, i_dw, x), want)
+    # entry conv with a -0.0 bias entry: the per-tap entry kernel, exact
+    E = net.layers[0]
+    E.bias = E.bias.copy()
+    E.bias[0] = -0.0
+    E.weights = np.abs(E.weights).astype(np.float32)
+    xe = np.zeros((2, E.in_h, E.in_w, E.cin), np.float32)
+    want = _ref_layer(ref, net, 0, xe)
+    assert _same_bits(_run_layer(net, 0, xe), want)
