@@ -540,7 +540,76 @@ __global__ void dense_strict_kernel(const float* __restrict__ w, const float* __
     }
 }
 
-// SPCV_DW_PAIR=0: always the per-tap (skipping) entry / depthwise kernels.
+// Strict dense 1x1, f32x2 version: a CTA computes 32 rows x 64 columns, a
+// thread 4 rows x the column pair (n0 + tx, n0 + 32 + tx) as f32x2
+// accumulators; per output the order is bias, then k ascending with every
+// weight (zeros included), mul.rn then add.rn (fma.rn.f32x2(acc, 1.0, p)), as
+// dense_gemm_into / matmul_reference. k is staged by 32 in shared memory.
+__global__ void __launch_bounds__(256) dense_strict_pair_kernel(const float* __restrict__ w, const float* __restrict__ act,
+                                                                const float* __restrict__ bias, float* __restrict__ out,
+                                                                int M, int K, long long N, int S, int act_kind, float lo,
+                                                                float hi, unsigned long long one) {
+    __shared__ float ws[32][33];  // [row][k]
+    __shared__ float xs[32][65];  // [k][column]
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const long long n0 = blockIdx.x * 64LL;
+    const int r0 = blockIdx.y * 32;
+    unsigned long long acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int r = r0 + 4 * ty + q;
+        const float b = (bias && r < M) ? bias[r] : 0.0f;
+        acc[q] = pk2(b, b);
+    }
+    const float* xcol[8];  // this thread's staging columns n0 + ty + 8q (null past N)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const long long n = n0 + ty + 8 * q;
+        const long long img = n / S, s = n - img * S;
+        xcol[q] = n < N ? act + img * K * S + s : nullptr;
+    }
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + tx;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int rr = ty + 8 * q, r = r0 + rr;
+            ws[rr][tx] = (r < M && k < K) ? w[static_cast<long long>(r) * K + k] : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            xs[tx][ty + 8 * q] = (xcol[q] && k < K) ? xcol[q][static_cast<long long>(k) * S] : 0.0f;
+        __syncthreads();
+        const int kn = min(32, K - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+            const unsigned long long x = pk2(xs[kk][tx], xs[kk][32 + tx]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float wv = ws[4 * ty + q][kk];
+                unsigned long long p;
+                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(pk2(wv, wv)), "l"(x));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(acc[q]) : "l"(acc[q]), "l"(one), "l"(p));
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const long long n = n0 + tx + 32 * h;
+        if (n >= N) continue;
+        const long long img = n / S, s = n - img * S;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + 4 * ty + q;
+            if (r >= M) continue;
+            float e0, e1;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(e0), "=f"(e1) : "l"(acc[q]));
+            out[(img * M + r) * S + s] = act_apply(h ? e1 : e0, act_kind, lo, hi);
+        }
+    }
+}
+
+// SPCV_DW_PAIR=0: always the per-tap (skipping) entry / depthwise kernels and
+// the scalar strict dense kernel.
 bool pair_off() {
     static const bool off = [] {
         const char* e = std::getenv("SPCV_DW_PAIR");
@@ -745,9 +814,16 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
                 } else {
                     const long long N = static_cast<long long>(images) * L.in_h * L.in_w;
                     dim3 grid(blocks_for(N, 32), static_cast<unsigned>((L.rows + 31) / 32));
-                    dense_strict_kernel<<<grid, dim3(32, 8), 0, st>>>(m->d_dense[i], cur, m->d_bias[i], dst,
-                                                                      L.rows, L.cols, N, L.in_h * L.in_w,
-                                                                      L.act_kind, L.lo, L.hi);
+                    if (pair_off()) {
+                        dense_strict_kernel<<<grid, dim3(32, 8), 0, st>>>(m->d_dense[i], cur, m->d_bias[i], dst,
+                                                                          L.rows, L.cols, N, L.in_h * L.in_w,
+                                                                          L.act_kind, L.lo, L.hi);
+                    } else {
+                        const dim3 pgrid(blocks_for(N, 64), static_cast<unsigned>((L.rows + 31) / 32));
+                        dense_strict_pair_kernel<<<pgrid, dim3(32, 8), 0, st>>>(
+                            m->d_dense[i], cur, m->d_bias[i], dst, L.rows, L.cols, N, L.in_h * L.in_w, L.act_kind,
+                            L.lo, L.hi, 0x3f8000003f800000ULL);
+                    }
                     g_launches.fetch_add(1, std::memory_order_relaxed);
                 }
                 break;
