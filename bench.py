@@ -485,6 +485,17 @@ def main():
                                                 max(dom["alg_bytes"] / (hbm_peak * 1e9),
                                                     dom["flops"] / (gather_roof * 1e12 * dom["bh"]))), 4),
                     "gather_frac": round(dom["gflops"] / 1e3 / gather_roof, 4),
+                    # every layer of the step against its roofs: the tile kernel is bound by
+                    # the lower of HBM and the shared-memory gather; the weight-specialised
+                    # (spcv_jit) kernels gather nothing (activations in registers): HBM only
+                    "layers": {p["name"]: {
+                        "kernel": p["kernel"], "us": round(p["us"], 1),
+                        "bound": "hbm" if p["kernel"] == "spcv_jit" or p["alg_bytes"] / (hbm_peak * 1e9) >=
+                                 p["flops"] / (gather_roof * 1e12 * p["bh"]) else "gather",
+                        "hbm_frac": round(p["hbm_frac"], 4),
+                        "gather_frac": (None if p["kernel"] == "spcv_jit" else
+                                        round(p["gflops"] / 1e3 / (gather_roof * p["bh"]), 4))}
+                        for p in per_layer},
                     "step_gather_frac": round(value / 1e3 / dist.world / gather_roof, 4),
                     "note": "achieved = SURVEY.md §8d algorithmic bytes / CUDA-event launch time. "
                             "Layers with AI > ~2.9 FLOP/B are bound by the shared-memory gather roof "
