@@ -198,8 +198,26 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     const char* env_tail = std::getenv("SPCV_TAIL");
     if (full_rounds >= 1 && left > 0 && !(env_tail && std::atoi(env_tail) == 0)) {
         int ts = 1;
-        while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
-        if (ts > 1) {
+        if (per_sm == 1) {
+            // One CTA per SM (K ~ 1024): split the partial round's tiles ts ways
+            // (row slices) where that shortens it most: ceil(left * ts / sms)
+            // sub-rounds of 1/ts of a tile, plus kStage of a tile per staging.
+            // (measured: MBv1 pw13 242.9 -> 232.0 us at 4 slices; 8 slices lose:
+            // pw13 +17 %, c5 +4 %)
+            constexpr double kStage = 0.05;
+            double best = 1.0 + kStage;
+            for (int t = 2; t <= 4 && g.nwarps * g.split * t <= kBins; t *= 2) {
+                const double rounds = static_cast<double>((left * t + resident - 1) / resident);
+                const double cost = rounds * (1.0 / t + kStage);
+                if (cost < best - 1e-9) best = cost, ts = t;
+            }
+        } else {
+            // several CTAs share each SM: split while the tail stays under 3/4
+            // of a round (measured best for the 2-3 CTA/SM layers)
+            while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
+        }
+        if (env_tail && std::atoi(env_tail) > 1) ts = std::atoi(env_tail);  // tuning aid
+        if (ts > 1 && g.nwarps * g.split * ts <= kBins) {
             g.tail_split = ts;
             g.tail_start = ntiles - left / g.split;
         }
