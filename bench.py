@@ -170,8 +170,10 @@ def main():
 
     import torch
 
-    dist = Dist("nccl")
-    dev = dist.local
+    # SPCV_DIST_BACKEND=gloo runs the N>1 code path with ranks sharing a GPU
+    # (a functional check on a one-GPU box; NCCL refuses two ranks per GPU)
+    dist = Dist(os.environ.get("SPCV_DIST_BACKEND", "nccl"))
+    dev = dist.local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     import paper_1911_09723_b200 as sp
 
