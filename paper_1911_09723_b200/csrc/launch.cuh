@@ -26,6 +26,16 @@ struct Geometry {
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
 
+// The geometry knobs (SPCV_NWARPS, SPCV_SPLIT, SPCV_TAIL) as one cache-key value.
+inline long long geometry_env_key() {
+    long long key = 0;
+    for (const char* name : {"SPCV_NWARPS", "SPCV_SPLIT", "SPCV_TAIL"}) {
+        const char* e = std::getenv(name);
+        key = key * 64 + (e ? (std::atoi(e) & 31) + 1 : 0);
+    }
+    return key;
+}
+
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                  cudaStream_t st) {
@@ -40,13 +50,14 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
                                        static_cast<int>(kSmemLimit)));
         configured.fetch_or(bit);
     }
-    // Geometry depends only on (kernel, weights, tile count): cache the last one.
-    static thread_local long long key[5] = {-1, -1, -1, -1, -1};
+    // Geometry depends only on (kernel, weights, tile count) and the tuning
+    // knobs: cache the last one.
+    static thread_local long long key[6] = {-1, -1, -1, -1, -1, -1};
     static thread_local Geometry g;
-    const long long k[5] = {ntiles, dev, w->cols, w->rows, w->T};
-    if (!std::equal(k, k + 5, key)) {
+    const long long k[6] = {ntiles, dev, w->cols, w->rows, w->T, geometry_env_key()};
+    if (!std::equal(k, k + 6, key)) {
         g = geometry(kern, w, ntiles, sms);
-        std::copy(k, k + 5, key);
+        std::copy(k, k + 6, key);
     }
     dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
     spcvk::KernelArgs at = a;

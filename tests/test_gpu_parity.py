@@ -750,3 +750,25 @@ def test_randomized_shapes_bit_exact(oracle, monkeypatch, kernel):
         got = run_device(m, act, bias, fused, dw=dw)
         want = oracle.spmm(m, act, bias, fused).reshape(got.shape)
         assert np.array_equal(bits(got), bits(want)), (case, K, M, bh, H, W, B, sparsity)
+
+
+# ------------------------------------ launch geometry: tail and row splits
+@pytest.mark.parametrize("env", [{"SPCV_TAIL": "0"}, {"SPCV_TAIL": "2"}, {"SPCV_TAIL": "4"}, {"SPCV_TAIL": "8"},
+                                 {"SPCV_SPLIT": "2", "SPCV_TAIL": "4"}, {"SPCV_NWARPS": "8", "SPCV_TAIL": "8"},
+                                 {"SPCV_SPLIT": "4"}], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("case", [
+    ("k1024", Layer("k1024", 1024, 256, 7, 7, sparsity=0.9), 120),          # one CTA per SM, 184 tiles
+    ("skew", Layer("skew", 512, 512, 7, 7, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.9, 1, True), 200),
+], ids=lambda c: c[0])
+def test_tail_and_row_splits_bit_exact(oracle, monkeypatch, env, case):
+    """The partial last round of tiles split 2/4/8 ways by rows (tail split),
+    every tile split across CTAs (SPCV_SPLIT), other CTA sizes: the LPT bins
+    each CTA takes change, the per-row arithmetic does not (bit-exact)."""
+    monkeypatch.setenv("SPCV_JIT", "0")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, layer, images = case
+    d = make_layer_data(layer, images, 99)
+    got = run_device(d.weights, d.act, d.bias, layer.act)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
