@@ -195,7 +195,12 @@ int spcv_cu_model_run(const spcv_cu_model* m, int i, const float* act, int image
  * stream order on `stream`, with a stream-ordered workspace. In
  * SPCV_MODE_STRICT the logits are bit-identical to the reference's
  * run_network; SPCV_MODE_FAST uses fused multiply-adds (SpMM, entry and
- * depthwise convolutions) and cuBLAS for dense 1x1 layers. Input dims other than the model's -> SPCV_ERR_SHAPE
+ * depthwise convolutions) and cuBLAS for dense 1x1 layers. Serving: a call
+ * repeated with the same (images <= 16, input, logits, mode) on the same
+ * non-default stream is captured once into a CUDA graph (over a persistent
+ * workspace kept until spcv_cu_model_free) and replayed from then on;
+ * SPCV_MODEL_GRAPH=0 disables it, a stream that is already capturing gets
+ * plain launches. Input dims other than the model's -> SPCV_ERR_SHAPE
  * (check_run_inputs, netdef.cpp:433-441). */
 int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images, int in_h,
                           int in_w, int in_c, float* logits, int mode, void* stream);

@@ -296,10 +296,12 @@ void free_model(spcv_cu_model* m) {
     for (float* p : m->d_dense) cudaFree(p);
     for (float* p : m->d_bias) cudaFree(p);
     for (float* p : m->d_conv) cudaFree(p);
-    if (m->pool) {
-        cudaDeviceSynchronize();  // no forward may still hold workspace
-        cudaMemPoolDestroy(m->pool);
+    if (m->pool || !m->graphs.empty()) cudaDeviceSynchronize();  // no forward may still run
+    for (auto& g : m->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (float* p : g.ws) cudaFree(p);
     }
+    if (m->pool) cudaMemPoolDestroy(m->pool);
     delete m;
 }
 

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <deque>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -64,5 +66,19 @@ struct spcv_cu_model {
     // forward() workspace: a stream-ordered pool owned by the model that keeps
     // its memory between calls (no re-mapping per forward)
     cudaMemPool_t pool = nullptr;
+    // forward() replayed as a CUDA graph per (images, input, logits, mode,
+    // stream) for small batches (network.cu)
+    struct GraphEntry {
+        int images = 0, mode = 0, uses = 0;
+        const float* input = nullptr;
+        float* logits = nullptr;
+        cudaStream_t stream = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        bool failed = false;
+        uint64_t launches = 0;
+        std::vector<float*> ws;  // persistent workspace the graph reads and writes
+    };
+    mutable std::mutex graph_mu;
+    mutable std::deque<GraphEntry> graphs;
 };
 

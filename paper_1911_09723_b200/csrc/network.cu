@@ -703,24 +703,15 @@ int run_spatial_layer(const spcv_cu_model* m, size_t i, const float* in, int ima
 
 }  // namespace spcv_model
 
-extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images,
-                                     int in_h, int in_w, int in_c, float* logits, int mode,
-                                     void* stream) {
-    if (!m) return fail(SPCV_ERR_INVALID, "model: null model");
-    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
-        return fail(SPCV_ERR_INVALID, "model: unknown arithmetic mode");
-    const Net& net = m->net;
-    // check_run_inputs (netdef.cpp:433-441)
-    if (images < 0 || in_c != net.input_c || in_h != net.input_h || in_w != net.input_w)
-        return fail(SPCV_ERR_SHAPE, "run: input must be HWC " + std::to_string(net.input_h) + "x" +
-                                        std::to_string(net.input_w) + "x" + std::to_string(net.input_c));
-    if (images == 0) return SPCV_OK;
-    if (!input || !logits) return fail(SPCV_ERR_INVALID, "model: null tensor pointer");
-    int dev = 0;
-    SPCV_CUDA(cudaGetDevice(&dev));
-    if (dev != m->device) return fail(SPCV_ERR_INVALID, "model: loaded on another device");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+namespace {
 
+// The forward pass on stream st. ws == nullptr: a stream-ordered workspace
+// from the model's pool, freed at the end; else a persistent workspace
+// (cudaMalloc'd on first use into *ws, reused after) — what a captured graph
+// needs (no allocation inside the capture).
+int forward_impl(const spcv_cu_model* m, const float* input, int images, float* logits, int mode,
+                 cudaStream_t st, std::vector<float*>* ws) {
+    const Net& net = m->net;
     const size_t n = net.layers.size();
     std::vector<char> save(n, 0);
     for (const Layer& L : net.layers)
@@ -730,9 +721,19 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
         max_elems = std::max(max_elems, static_cast<size_t>(L.cout) * L.out_h * L.out_w);
     const size_t per_buf = max_elems * static_cast<size_t>(images) * sizeof(float);
 
-    // Stream-ordered workspace: two ping-pong buffers + one per residual source.
+    // Workspace: two ping-pong buffers + one per residual source.
     std::vector<float*> owned;
+    size_t next = 0;  // persistent workspace: buffers in allocation order
     auto alloc = [&](size_t bytes, float** p) -> int {
+        if (ws) {
+            if (next == ws->size()) {
+                float* q = nullptr;
+                SPCV_CUDA(cudaMalloc(reinterpret_cast<void**>(&q), std::max<size_t>(bytes, 4)));
+                ws->push_back(q);
+            }
+            *p = (*ws)[next++];
+            return SPCV_OK;
+        }
         SPCV_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 4), m->pool, st));
         owned.push_back(*p);
         return SPCV_OK;
@@ -843,4 +844,106 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
     }
     release();
     return rc;
+}
+
+// Replays of a captured forward (serving): a forward issued again with the same
+// (images, input, logits, mode, stream) is captured into a
+// CUDA graph over a persistent workspace and replayed from then on (one graph
+// launch instead of ~30 kernel launches). Only for batches up to
+// SPCV_MODEL_GRAPH_MAX_IMAGES (default 16: the persistent workspace of a
+// cached batch stays allocated until spcv_cu_model_free) and non-default
+// streams; SPCV_MODEL_GRAPH=0 disables it. A failed capture falls back to
+// plain launches for that key.
+int graph_max_images() {
+    static const int v = [] {
+        const char* off = std::getenv("SPCV_MODEL_GRAPH");
+        if (off && std::atoi(off) == 0) return 0;
+        const char* e = std::getenv("SPCV_MODEL_GRAPH_MAX_IMAGES");
+        return e ? std::atoi(e) : 16;
+    }();
+    return v;
+}
+
+}  // namespace
+
+extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input, int images,
+                                     int in_h, int in_w, int in_c, float* logits, int mode,
+                                     void* stream) {
+    if (!m) return fail(SPCV_ERR_INVALID, "model: null model");
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "model: unknown arithmetic mode");
+    const Net& net = m->net;
+    // check_run_inputs (netdef.cpp:433-441)
+    if (images < 0 || in_c != net.input_c || in_h != net.input_h || in_w != net.input_w)
+        return fail(SPCV_ERR_SHAPE, "run: input must be HWC " + std::to_string(net.input_h) + "x" +
+                                        std::to_string(net.input_w) + "x" + std::to_string(net.input_c));
+    if (images == 0) return SPCV_OK;
+    if (!input || !logits) return fail(SPCV_ERR_INVALID, "model: null tensor pointer");
+    int dev = 0;
+    SPCV_CUDA(cudaGetDevice(&dev));
+    if (dev != m->device) return fail(SPCV_ERR_INVALID, "model: loaded on another device");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread || images > graph_max_images())
+        return forward_impl(m, input, images, logits, mode, st, nullptr);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SPCV_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone)  // the caller is capturing: plain launches into its graph
+        return forward_impl(m, input, images, logits, mode, st, nullptr);
+
+    std::lock_guard<std::mutex> lk(m->graph_mu);
+    spcv_cu_model::GraphEntry* e = nullptr;
+    for (auto& g : m->graphs)
+        if (g.images == images && g.input == input && g.logits == logits && g.mode == mode && g.stream == st) e = &g;
+    if (!e) {
+        constexpr size_t kMaxGraphs = 4;  // oldest entry evicted (its stream drained first)
+        if (m->graphs.size() == kMaxGraphs) {
+            spcv_cu_model::GraphEntry& old = m->graphs.front();
+            cudaStreamSynchronize(old.stream);
+            if (old.exec) cudaGraphExecDestroy(old.exec);
+            for (float* p : old.ws) cudaFree(p);
+            m->graphs.pop_front();
+        }
+        m->graphs.emplace_back();
+        e = &m->graphs.back();
+        e->images = images;
+        e->input = input;
+        e->logits = logits;
+        e->mode = mode;
+        e->stream = st;
+    }
+    if (e->exec) {
+        SPCV_CUDA(cudaGraphLaunch(e->exec, st));
+        g_launches.fetch_add(e->launches, std::memory_order_relaxed);
+        return SPCV_OK;
+    }
+    if (e->failed || e->uses < 1) {
+        // 1st call: plain launches (kernels compiled and configured, the
+        // persistent workspace allocated); from the 2nd on: the graph
+        const int rc = forward_impl(m, input, images, logits, mode, st, e->failed ? nullptr : &e->ws);
+        if (rc == SPCV_OK) ++e->uses;
+        return rc;
+    }
+    const uint64_t n0 = g_launches.load();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    int rc = ce == cudaSuccess ? forward_impl(m, input, images, logits, mode, st, &e->ws) : SPCV_ERR_CUDA;
+    if (ce == cudaSuccess) {
+        const cudaError_t ee = cudaStreamEndCapture(st, &graph);
+        if (ee != cudaSuccess) rc = SPCV_ERR_CUDA;
+    }
+    if (rc == SPCV_OK && graph && cudaGraphInstantiate(&e->exec, graph, 0) != cudaSuccess) {
+        e->exec = nullptr;
+        rc = SPCV_ERR_CUDA;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();  // a failed capture leaves a sticky-free error behind
+    e->launches = g_launches.load() - n0;
+    if (rc != SPCV_OK || !e->exec) {
+        e->failed = true;
+        return forward_impl(m, input, images, logits, mode, st, nullptr);
+    }
+    g_launches.fetch_sub(e->launches, std::memory_order_relaxed);  // recorded, not launched
+    SPCV_CUDA(cudaGraphLaunch(e->exec, st));
+    g_launches.fetch_add(e->launches, std::memory_order_relaxed);
+    return SPCV_OK;
 }

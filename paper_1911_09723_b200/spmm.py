@@ -627,15 +627,18 @@ class DeviceModel:
                                      None if residual is None else residual.data_ptr(), out.data_ptr(),
                                      _capi.MODE_STRICT if strict else _capi.MODE_FAST, sptr))
 
-    def forward(self, images_hwc, strict: bool = True, stream=None):
+    def forward(self, images_hwc, strict: bool = True, stream=None, out=None):
         """run_network on the device: torch CUDA [B][H][W][C] fp32 -> logits [B][classes]
-        (spcv_cu_model_forward; bit-exact with the reference executor in strict mode)."""
+        (spcv_cu_model_forward; bit-exact with the reference executor in strict mode).
+        `out`: optional preallocated logits (a forward repeated with the same
+        input/output tensors on a non-default stream replays a CUDA graph)."""
         import torch
 
         x = images_hwc.contiguous()
         B, H, W, C = x.shape
         classes = self.layers[-1]["cout"]
-        out = torch.empty((B, classes), dtype=torch.float32, device=x.device)
+        if out is None:
+            out = torch.empty((B, classes), dtype=torch.float32, device=x.device)
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream

@@ -322,3 +322,40 @@ def test_spatial_layers_signed_zero_and_nonfinite_weights(ref):
     xe = np.zeros((2, E.in_h, E.in_w, E.cin), np.float32)
     want = _ref_layer(ref, net, 0, xe)
     assert _same_bits(_run_layer(net, 0, xe), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_forward_graph_replay_matches_run_network(ref, files, mode):
+    """A forward repeated with the same tensors on a non-default stream is
+    captured once and replayed as a CUDA graph: every replay reads the input's
+    current contents and stays bit-identical to the reference run_network
+    (strict) / matches the plain launches (fast), and counts the same launches."""
+    import torch
+
+    data = files["ours-mbv1-0.25"]
+    m = sp.DeviceModel(data)
+    L0 = m.layers[0]
+    rng = np.random.default_rng(17)
+    x = torch.empty((2, L0["in_h"], L0["in_w"], L0["cin"]), device="cuda")
+    out = torch.empty((2, m.layers[-1]["cout"]), device="cuda")
+    s = torch.cuda.Stream()
+    strict = mode == "strict"
+    counts = []
+    for it in range(5):
+        xh = rng.uniform(-1, 1, tuple(x.shape)).astype(np.float32)
+        x.copy_(torch.from_numpy(xh))
+        torch.cuda.synchronize()
+        n0 = sp.launch_count()
+        with torch.cuda.stream(s):
+            m.forward(x, strict, s, out=out)
+        s.synchronize()
+        counts.append(sp.launch_count() - n0)
+        got = out.cpu().numpy()
+        if strict:
+            want = ref.run_model(data, xh)
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), it
+        else:
+            plain = m.forward(torch.from_numpy(xh).cuda(), False).cpu().numpy()  # default stream: no graph
+            assert np.allclose(got, plain, rtol=1e-5, atol=1e-6), it
+    assert len(set(counts)) == 1 and counts[0] > 10, counts
