@@ -24,7 +24,7 @@ struct Geometry {
 };
 
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms);
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref);
 
 // The geometry knobs (SPCV_NWARPS, SPCV_SPLIT, SPCV_TAIL) as one cache-key value.
 inline long long geometry_env_key() {
@@ -52,12 +52,12 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     }
     // Geometry depends only on (kernel, weights, tile count) and the tuning
     // knobs: cache the last one.
-    static thread_local long long key[6] = {-1, -1, -1, -1, -1, -1};
+    static thread_local long long key[7] = {-1, -1, -1, -1, -1, -1, -2};
     static thread_local Geometry g;
-    const long long k[6] = {ntiles, dev, w->cols, w->rows, w->T, geometry_env_key()};
-    if (!std::equal(k, k + 6, key)) {
-        g = geometry(kern, w, ntiles, sms);
-        std::copy(k, k + 6, key);
+    const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, geometry_env_key(), a.tail_pref};
+    if (!std::equal(k, k + 7, key)) {
+        g = geometry(kern, w, ntiles, sms, a.tail_pref);
+        std::copy(k, k + 7, key);
     }
     dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
     spcvk::KernelArgs at = a;
@@ -172,7 +172,7 @@ int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt
 // each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
 // split tiles across CTAs (row split) until the grid covers the GPU.
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms) {
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref) {
     Geometry g;
     g.ntiles = ntiles;
     g.smem = smem_bytes(w->cols, w->rows, w->T);
@@ -227,6 +227,7 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
             // of a round (measured best for the 2-3 CTA/SM layers)
             while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
         }
+        if (tail_pref >= 0) ts = std::max(1, tail_pref);                      // autotuned (spcv_cu.cu)
         if (env_tail && std::atoi(env_tail) > 1) ts = std::atoi(env_tail);  // tuning aid
         if (ts > 1 && g.nwarps * g.split * ts <= kBins) {
             g.tail_split = ts;

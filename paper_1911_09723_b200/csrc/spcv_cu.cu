@@ -476,6 +476,61 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
     return SPCV_OK;
 }
 
+// Autotuned tail split. The last, partial round of column tiles can run
+// unsplit or split 2 or 4 ways by rows; which is fastest depends on the
+// layer (measured: c3 at 2-3 tiles per SM 7 % faster unsplit, MBv1 pw12 at
+// the same tile count 25 % slower), and every choice gives the same bits (the
+// per-row arithmetic does not depend on the split). The first call of a
+// (weights, columns, mode, layout) shape times the candidates with events on
+// its stream (two launches each after one warm-up) and caches the winner in
+// the weights. Skipped (heuristic) when SPCV_AUTOTUNE=0 or SPCV_TAIL is set,
+// with a residual (a repeated launch must not re-add it), or while the stream
+// is being captured.
+template <typename Run>
+int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, bool strict, bool vec,
+               cudaStream_t st, Run&& run) {
+    const char* env = std::getenv("SPCV_AUTOTUNE");
+    if ((env && std::atoi(env) == 0) || std::getenv("SPCV_TAIL") != nullptr || a.residual) return -1;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return -1;
+    const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
+    auto* mw = const_cast<spcv_cu_weights*>(w);
+    {
+        std::lock_guard<std::mutex> lk(mw->tune_mu);
+        for (const auto& kv : mw->tuned_tail)
+            if (kv.first == key) return kv.second;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        if (e0) cudaEventDestroy(e0);
+        return -1;
+    }
+    int best = -1;
+    float best_ms = 0.0f;
+    uint64_t runs = 0;  // tuning launches are not the caller's work: not counted
+    for (int cand : {-1, 0, 2, 4}) {
+        spcvk::KernelArgs t = a;
+        t.tail_pref = cand;
+        if (run(t) != SPCV_OK) continue;  // warm-up (geometry, L2)
+        ++runs;
+        cudaEventRecord(e0, st);
+        const int r1 = run(t), r2 = run(t);
+        runs += (r1 == SPCV_OK) + (r2 == SPCV_OK);
+        cudaEventRecord(e1, st);
+        float ms = 0.0f;
+        if (r1 != SPCV_OK || r2 != SPCV_OK || cudaEventSynchronize(e1) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess)
+            continue;
+        if (best_ms == 0.0f || ms < best_ms * 0.98f) best = cand, best_ms = ms;  // 2 %: stay with the heuristic on ties
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    g_launches.fetch_sub(runs, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(mw->tune_mu);
+    mw->tuned_tail.emplace_back(key, best);
+    return best;
+}
+
 int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, int act_w,
            const float* bias, int act_kind, float lo, float hi, float* out, int mode,
            cudaStream_t st, int out_rows = -1, const float* residual = nullptr) {
@@ -509,6 +564,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.hi = hi;
     a.tail_start = 0x7FFFFFFFFFFFFFFFLL;
     a.tail_split = 1;
+    a.tail_pref = -1;
     a.one2 = 0x3f8000003f800000ULL;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
@@ -547,11 +603,15 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
             if (v->direct || N >= min_cols) return jit_launch(v, a, st);
         }
     }
-    switch (w->block_h) {
-        case 1: return launch_bh1(a, w, ntiles, sms, strict, vec, st);
-        case 2: return launch_bh2(a, w, ntiles, sms, strict, vec, st);
-        default: return launch_bh4(a, w, ntiles, sms, strict, vec, st);
-    }
+    auto run = [&](const spcvk::KernelArgs& args) {
+        switch (w->block_h) {
+            case 1: return launch_bh1(args, w, ntiles, sms, strict, vec, st);
+            case 2: return launch_bh2(args, w, ntiles, sms, strict, vec, st);
+            default: return launch_bh4(args, w, ntiles, sms, strict, vec, st);
+        }
+    };
+    a.tail_pref = tuned_tail(w, a, N, strict, vec, st, run);
+    return run(a);
 }
 
 // Per-thread device scratch and streams of the host-tensor entry point:

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <deque>
 #include <cstddef>
+#include <mutex>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -78,6 +79,9 @@ struct spcv_cu_weights {
     std::vector<uint32_t> h_row_ptr, h_col_idx;
     std::vector<float> h_values;
     std::deque<JitVariant> jit;  // deque: variants never move (launching threads hold pointers)
+    // autotuned tail split per call shape (spcv_cu.cu: tuned_tail)
+    std::mutex tune_mu;
+    std::vector<std::pair<long long, int>> tuned_tail;
 };
 
 namespace spcv_detail {

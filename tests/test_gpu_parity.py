@@ -772,3 +772,26 @@ def test_tail_and_row_splits_bit_exact(oracle, monkeypatch, env, case):
     got = run_device(d.weights, d.act, d.bias, layer.act)
     want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
     assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("case", [
+    ("c3_bh4", Layer("c3", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.9, 4), 64),
+    ("pw12", Layer("pw12", 512, 1024, 7, 7, sparsity=0.9), 256),
+], ids=lambda c: c[0])
+def test_autotuned_tail_split_bit_exact_and_uncounted(oracle, monkeypatch, case):
+    """The first call of a shape times the tail-split candidates (spcv_cu.cu:
+    tuned_tail): its result, the cached choice on later calls and the untuned
+    heuristic (SPCV_AUTOTUNE=0) are bit-identical to the oracle, and each call
+    counts as one launch (the tuning launches are internal)."""
+    monkeypatch.setenv("SPCV_JIT", "0")
+    _, layer, images = case
+    d = make_layer_data(layer, images, 7)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8)
+    for tune in ("1", "0"):
+        monkeypatch.setenv("SPCV_AUTOTUNE", tune)
+        dw = sp.DeviceBcsr(d.weights)  # fresh weights: no cached choice
+        for _ in range(2):
+            n0 = sp.launch_count()
+            got = run_device(d.weights, d.act, d.bias, layer.act, dw=dw)
+            assert sp.launch_count() == n0 + 1
+            assert np.array_equal(bits(got), bits(want.reshape(got.shape)))
