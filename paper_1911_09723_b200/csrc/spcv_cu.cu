@@ -483,23 +483,25 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
 // per-row arithmetic does not depend on the split). The first call of a
 // (weights, columns, mode, layout) shape times the candidates with events on
 // its stream (two launches each after one warm-up) and caches the winner in
-// the weights. Skipped (heuristic) when SPCV_AUTOTUNE=0 or SPCV_TAIL is set,
-// with a residual (a repeated launch must not re-add it), or while the stream
-// is being captured.
+// the weights. Not tuned (heuristic) when SPCV_AUTOTUNE=0 or SPCV_TAIL is set;
+// a shape first seen with a residual (a repeated launch would re-add it into
+// an aliased output) or inside a stream capture uses the heuristic until an
+// eligible call has tuned it.
 template <typename Run>
 int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, bool strict, bool vec,
                cudaStream_t st, Run&& run) {
     const char* env = std::getenv("SPCV_AUTOTUNE");
-    if ((env && std::atoi(env) == 0) || std::getenv("SPCV_TAIL") != nullptr || a.residual) return -1;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return -1;
+    if ((env && std::atoi(env) == 0) || std::getenv("SPCV_TAIL") != nullptr) return -1;
     const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
     auto* mw = const_cast<spcv_cu_weights*>(w);
     {
         std::lock_guard<std::mutex> lk(mw->tune_mu);
         for (const auto& kv : mw->tuned_tail)
-            if (kv.first == key) return kv.second;
+            if (kv.first == key) return kv.second;  // also inside a capture / with a residual
     }
+    if (a.residual) return -1;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return -1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
         if (e0) cudaEventDestroy(e0);
