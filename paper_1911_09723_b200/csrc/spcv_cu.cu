@@ -484,9 +484,9 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
 // (weights, columns, mode, layout) shape times the candidates with events on
 // its stream (two launches each after one warm-up) and caches the winner in
 // the weights. Not tuned (heuristic) when SPCV_AUTOTUNE=0 or SPCV_TAIL is set;
-// a shape first seen with a residual (a repeated launch would re-add it into
-// an aliased output) or inside a stream capture uses the heuristic until an
-// eligible call has tuned it.
+// a shape first seen with an output overlapping its residual (a repeated
+// launch would re-add it) or inside a stream capture uses the heuristic until
+// an eligible call has tuned it.
 template <typename Run>
 int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, bool strict, bool vec,
                cudaStream_t st, Run&& run) {
@@ -499,7 +499,12 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
         for (const auto& kv : mw->tuned_tail)
             if (kv.first == key) return kv.second;  // also inside a capture / with a residual
     }
-    if (a.residual) return -1;
+    if (a.residual) {  // repeated launches are idempotent unless out overlaps the residual
+        const size_t bytes = static_cast<size_t>(N / a.S) * a.M_out * a.S * sizeof(float);
+        const char* r0 = reinterpret_cast<const char*>(a.residual);
+        const char* o0 = reinterpret_cast<const char*>(a.out);
+        if (r0 < o0 + bytes && o0 < r0 + bytes) return -1;
+    }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return -1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
