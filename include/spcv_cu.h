@@ -88,7 +88,8 @@ int spcv_cu_weights_info(const spcv_cu_weights* w, int* rows, int* cols, int* bl
 void spcv_cu_free(spcv_cu_weights* w);
 
 /* Which CUDA kernel spmm runs for these weights in `mode`:
- *   SPCV_KERNEL_TILE — the shared-memory tile kernel (any K up to the tile limit);
+ *   SPCV_KERNEL_TILE — the shared-memory tile kernel (any K: wide matrices run
+ *                      as channel passes that continue each other's sums);
  *   SPCV_KERNEL_JIT  — a kernel specialised on this matrix's structure and
  *                      values (weights as instruction immediates), compiled
  *                      with NVRTC on first use and cached in the weights:

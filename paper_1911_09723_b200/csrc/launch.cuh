@@ -126,7 +126,8 @@ int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt,
     const int ns = vec ? pipe_stages(w) : 0;
     const char* env = std::getenv("SPCV_PIPELINE");
     // Opt-in for now: with 8 consumer warps it trails the tile kernel (profiles/).
-    const bool pipe = ns >= 2 && ((env && std::atoi(env) != 0) || kind == "pipe");
+    const bool pipe = ns >= 2 && ((env && std::atoi(env) != 0) || kind == "pipe") && a.acc_in == nullptr &&
+                      a.K_img == a.K;  // channel passes: the tile kernel only
     if constexpr (STEPS == 4) {
         if (pipe)
             return strict ? launch_pipe<BH, LPR, NF, true>(a, w, nt, sms, ns, st)

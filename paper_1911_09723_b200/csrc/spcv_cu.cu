@@ -141,6 +141,7 @@ void free_weights(spcv_cu_weights* w) {
     cudaFree(w->d_bin_beg);
     cudaFree(w->d_stream_fast);
     cudaFree(w->d_bin_beg_fast);
+    for (spcv_cu_weights* p : w->parts) free_weights(p);
     jit_release(w);
     delete w;
 }
@@ -148,6 +149,76 @@ void free_weights(spcv_cu_weights* w) {
 }  // namespace
 
 // ------------------------------------------------------------------ packing
+
+namespace {
+
+// Input channels per pass when K is too wide for one [K][T] tile.
+constexpr int kPassChannels = 1024;
+
+// A matrix too wide for one shared-memory tile: packed as parts over channel
+// ranges [k0, k0 + kPassChannels), column indices rebased, every block row
+// present in every part (empty where it has no block in the range). The
+// paper-format streams of the whole matrix are kept for spcv_cu_unpack.
+int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const uint32_t* col_idx, size_t nblocks,
+                const float* values, spcv_cu_weights** out) {
+    const int brows = rows / block_h;
+    auto* w = new (std::nothrow) spcv_cu_weights;
+    if (!w) return fail(SPCV_ERR_CUDA, "spcv_cu_pack: out of host memory");
+    w->rows = rows;
+    w->cols = cols;
+    w->block_h = block_h;
+    w->brows = brows;
+    w->nblocks = nblocks;
+    cudaGetDevice(&w->device);
+    int rc = SPCV_OK;
+    for (int k0 = 0; k0 < cols && rc == SPCV_OK; k0 += kPassChannels) {
+        const uint32_t k1 = static_cast<uint32_t>(std::min(cols, k0 + kPassChannels));
+        std::vector<uint32_t> rp(static_cast<size_t>(brows) + 1, 0), ci;
+        std::vector<float> va;
+        for (int r = 0; r < brows; ++r) {
+            for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b)
+                if (col_idx[b] >= static_cast<uint32_t>(k0) && col_idx[b] < k1) {
+                    ci.push_back(col_idx[b] - static_cast<uint32_t>(k0));
+                    for (int i = 0; i < block_h; ++i) va.push_back(values[static_cast<size_t>(b) * block_h + i]);
+                }
+            rp[r + 1] = static_cast<uint32_t>(ci.size());
+        }
+        spcv_cu_weights* part = nullptr;
+        rc = spcv_cu_pack(rows, static_cast<int>(k1) - k0, block_h, rp.data(), rp.size(), ci.data(), ci.size(),
+                          va.data(), va.size(), &part);
+        if (rc == SPCV_OK) {
+            part->jit_eligible = false;  // passes run the tile kernel (it continues sums)
+            w->parts.push_back(part);
+            w->part_k0.push_back(k0);
+        }
+    }
+    if (rc == SPCV_OK) {
+        w->G = w->parts[0]->G;
+        w->LPR = w->parts[0]->LPR;
+        w->NF = w->parts[0]->NF;
+        w->T = w->parts[0]->T;
+        std::vector<uint32_t> nnz(brows), delta(nblocks);
+        for (int r = 0; r < brows; ++r) {
+            nnz[r] = row_ptr[r + 1] - row_ptr[r];
+            uint32_t prev = 0;
+            for (uint32_t b = row_ptr[r]; b < row_ptr[r + 1]; ++b) {
+                delta[b] = col_idx[b] - prev;
+                prev = col_idx[b];
+            }
+        }
+        if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) == SPCV_OK &&
+            (rc = upload(&w->d_delta, delta.data(), delta.size())) == SPCV_OK)
+            rc = upload(&w->d_values, values, nblocks * static_cast<size_t>(block_h));
+    }
+    if (rc != SPCV_OK) {
+        free_weights(w);
+        return rc;
+    }
+    *out = w;
+    return SPCV_OK;
+}
+
+}  // namespace
 
 extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row_ptr,
                             size_t row_ptr_len, const uint32_t* col_idx, size_t nblocks,
@@ -189,9 +260,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     }
 
     const Layout lay = choose_layout(cols, rows, block_h);
-    if (lay.LPR == 0 || cols >= 0xFFFF)
-        return fail(SPCV_ERR_UNSUPPORTED, "spcv_cu_pack: input channels " + std::to_string(cols) +
-                                              " exceed the shared-memory tile limit");
+    if (lay.LPR == 0 || cols >= 0xFFFF) return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out);
     const int G = 32 / lay.LPR;
     const int T = lay.T;
     const int BH = block_h;
@@ -499,6 +568,7 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
         for (const auto& kv : mw->tuned_tail)
             if (kv.first == key) return kv.second;  // also inside a capture / with a residual
     }
+    if (a.acc_in) return -1;  // a later channel pass reads out: not repeatable in place
     if (a.residual) {  // repeated launches are idempotent unless out overlaps the residual
         const size_t bytes = static_cast<size_t>(N / a.S) * a.M_out * a.S * sizeof(float);
         const char* r0 = reinterpret_cast<const char*>(a.residual);
@@ -540,12 +610,28 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
 
 int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, int act_w,
            const float* bias, int act_kind, float lo, float hi, float* out, int mode,
-           cudaStream_t st, int out_rows = -1, const float* residual = nullptr) {
+           cudaStream_t st, int out_rows = -1, const float* residual = nullptr,
+           const float* acc_in = nullptr, int k_img = -1) {
     const long long S = static_cast<long long>(act_h) * act_w;
     const long long N = S * images;
     if (N == 0) return SPCV_OK;
     if (S > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: spatial extent too large");
     if (!act || !out) return fail(SPCV_ERR_INVALID, "spmm: null tensor pointer");
+    if (!w->parts.empty()) {
+        // Channel passes in order: the first starts from the bias and stores raw
+        // sums into out, each next continues from out; the clamp and the
+        // residual belong to the last. Every output still sums its terms in the
+        // reference order (bias, channels ascending): bit-exact in strict mode.
+        const size_t P = w->parts.size();
+        for (size_t p = 0; p < P; ++p) {
+            const bool last = p + 1 == P;
+            const int rc = launch(w->parts[p], act + static_cast<long long>(w->part_k0[p]) * S, images, act_h,
+                                  act_w, p == 0 ? bias : nullptr, last ? act_kind : SPCV_ACT_NONE, lo, hi, out,
+                                  mode, st, out_rows, last ? residual : nullptr, p == 0 ? nullptr : out, w->cols);
+            if (rc != SPCV_OK) return rc;
+        }
+        return SPCV_OK;
+    }
     int dev = 0;
     SPCV_CUDA(cudaGetDevice(&dev));
     if (dev != w->device)
@@ -562,6 +648,8 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.steps = mode == SPCV_MODE_FAST ? w->STEPS_fast : w->STEPS;
     a.N = N;
     a.K = w->cols;
+    a.K_img = k_img < 0 ? w->cols : k_img;
+    a.acc_in = acc_in;
     a.M = w->rows;
     a.M_out = out_rows < 0 ? w->rows : out_rows;
     a.residual = residual;
@@ -578,7 +666,8 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     const int sms = props_for(dev).sms;
     const bool vec = (S % 4 == 0) && (reinterpret_cast<uintptr_t>(act) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
-                     (reinterpret_cast<uintptr_t>(residual) % 16 == 0);
+                     (reinterpret_cast<uintptr_t>(residual) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(acc_in) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
     if (w->jit_eligible) {
         // const_cast: the compiled kernel is a cache inside the weights object

@@ -79,6 +79,11 @@ struct spcv_cu_weights {
     std::vector<uint32_t> h_row_ptr, h_col_idx;
     std::vector<float> h_values;
     std::deque<JitVariant> jit;  // deque: variants never move (launching threads hold pointers)
+    // Channel passes (K too wide for one shared-memory tile): the matrix split
+    // by input-channel range, each part packed on its own; a call runs them in
+    // channel order, each continuing the previous part's sums (spcv_cu.cu)
+    std::vector<spcv_cu_weights*> parts;
+    std::vector<int> part_k0;
     // autotuned tail split per call shape (spcv_cu.cu: tuned_tail)
     std::mutex tune_mu;
     std::vector<std::pair<long long, int>> tuned_tail;

@@ -58,6 +58,9 @@ struct KernelArgs {
     long long N;             // images * S
     int K, M, S;             // M: weight rows (block rows * block_h)
     int M_out;               // rows stored (<= M): the executor's padded-row truncation
+    int K_img;               // channels between consecutive images of act (K, or more for a channel pass)
+    const float* acc_in;     // nullptr: accumulators start at the bias; else at acc_in ([images][M_out][S],
+                             // the previous channel pass's raw sums; may alias out)
     const float* residual;   // nullptr or [images][M_out][S], added after the activation
     int act_kind;            // 0 none, 1 clamp
     float lo, hi;
@@ -282,6 +285,37 @@ struct Exec {
         brow = kNoRow;
     }
 
+    // Accumulators of the new group from acc_in (channel passes): the exact
+    // fp32 running sums the previous pass stored (raw, before the clamp), so
+    // the terms keep arriving in the reference order. Rows past M_out (never
+    // stored) and columns past N start at 0.
+    __device__ __forceinline__ void load_acc(const KernelArgs& a) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const int col = static_cast<int>(lane_off[j] >> 2);
+#pragma unroll
+            for (int i = 0; i < BH; ++i) {
+                const int r = static_cast<int>(brow) * BH + i;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (brow != kNoRow && r < a.M_out) {
+                    const long long roff = static_cast<long long>(r) * a.S;
+                    if constexpr (VEC) {
+                        if (ocol[j] >= 0) v = *reinterpret_cast<const float4*>(a.acc_in + ocol[j] + roff);
+                    } else {
+                        float e[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const long long o = s_col[col + q];
+                            e[q] = o >= 0 ? a.acc_in[o + roff] : 0.0f;
+                        }
+                        v = make_float4(e[0], e[1], e[2], e[3]);
+                    }
+                }
+                acc[i][j] = v;
+            }
+        }
+    }
+
     // One chunk: a group header closes the previous group and opens the next;
     // a data chunk is STEPS unconditional steps. Padding steps point at the
     // zero row with weight -0.0f: acc + (-0.0f * +0.0f) == acc exactly for
@@ -290,6 +324,10 @@ struct Exec {
         if ((cur.ix[0] & kHeaderHi) == kHeaderHi) {
             finish(a);
             brow = cur.ix[0] & 0xFFFFu;
+            if (a.acc_in) {  // a later channel pass: continue the previous pass's sums
+                load_acc(a);
+                return;
+            }
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
                 const float b = (brow != kNoRow && have_bias) ? s_bias[brow * BH + i] : 0.0f;
@@ -382,7 +420,7 @@ __device__ __forceinline__ Chunk<BH, STEPS> zero_chunk() {
 template <int T, bool VEC>
 __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long long n0,
                                            const KernelArgs& a, int tid, int nthreads) {
-    const long long KS = static_cast<long long>(a.K) * a.S;
+    const long long KS = static_cast<long long>(a.K_img) * a.S;
     for (int c = tid; c < T; c += nthreads) s_col[c] = col_offset(n0 + c, a);
     if constexpr (VEC) {
         constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)

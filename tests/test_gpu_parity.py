@@ -442,11 +442,45 @@ def test_zero_images_is_a_noop():
     assert sp.launch_count() == n0
 
 
-def test_too_many_input_channels_is_reported():
-    w = np.zeros((4, 2000), np.float32)
-    w[0, 0] = 1
-    with pytest.raises(sp.DeviceError):
-        sp.DeviceBcsr(sp.encode_bcsr(w, 1))
+@pytest.mark.parametrize("case", [
+    ("k2000_id", 4, 2000, 1, 0.0, ("none", 0.0, 0.0), (3, 2), 2),
+    ("k1100", 64, 1100, 1, 0.9, ("clamp", 0.0, 6.0), (7, 7), 6),
+    ("k2048_bh4", 128, 2048, 4, 0.8, ("clamp", 0.0, float("inf")), (4, 4), 5),
+    ("k2500_bh2", 40, 2500, 2, 0.95, ("none", 0.0, 0.0), (3, 5), 4),
+    ("k3100_dense", 8, 3100, 1, 0.0, ("clamp", -1.0, 1.0), (2, 2), 3),
+], ids=lambda c: c[0])
+def test_wide_matrices_run_as_channel_passes_bit_exact(oracle, case):
+    """Input channels beyond one shared-memory tile (K > 1024 per pass) run as
+    channel passes that continue each other's sums (spcv_cu.cu: pack_passes):
+    strict results equal the oracle bit for bit (the reference order of terms
+    is kept across passes), fast ones stay within tolerance, and the packed
+    matrix still unpacks to the original BCSR."""
+    name, M, K, bh, sparsity, act, hw, images = case
+    rng = np.random.default_rng(K)
+    dense = (rng.standard_normal((M, K)) * 0.1).astype(np.float32)
+    if name == "k2000_id":
+        dense[:] = 0
+        dense[np.arange(M), np.arange(M) * 499] = 1.0  # picks channels 0, 499, 998, 1497
+    elif sparsity > 0:
+        keep = rng.random((M // bh, K)) >= sparsity
+        dense *= np.repeat(keep, bh, axis=0)
+    m = sp.encode_bcsr(dense, bh)
+    act_ = rng.uniform(-1, 1, (images, K) + hw).astype(np.float32)
+    bias = (rng.standard_normal(M) * 0.1).astype(np.float32)
+    got = run_device(m, act_, bias, act)
+    want = oracle.spmm(m, act_, bias, act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
+    if name == "k2000_id":
+        x = act_.reshape(images, K, -1)
+        ident = np.stack([x[:, 0], x[:, 499], x[:, 998], x[:, 1497]], 1) + bias[None, :, None]
+        assert np.array_equal(got.reshape(images, M, -1), ident.astype(np.float32))
+    fast = run_device(m, act_, bias, act, strict=False)
+    assert np.allclose(fast, want, rtol=1e-4, atol=1e-5)
+    u = sp.DeviceBcsr(m).unpack()
+    assert np.array_equal(np.asarray(u.row_ptr), np.asarray(m.row_ptr))
+    assert np.array_equal(np.asarray(u.col_idx), np.asarray(m.col_idx))
+    assert np.array_equal(np.asarray(u.values, np.float32).view(np.uint32),
+                          np.asarray(m.values, np.float32).view(np.uint32))
 
 
 def test_concurrent_streams_agree(oracle):
@@ -795,3 +829,28 @@ def test_autotuned_tail_split_bit_exact_and_uncounted(oracle, monkeypatch, case)
             got = run_device(d.weights, d.act, d.bias, layer.act, dw=dw)
             assert sp.launch_count() == n0 + 1
             assert np.array_equal(bits(got), bits(want.reshape(got.shape)))
+
+
+@pytest.mark.parametrize("hw", [(7, 9), (8, 8)], ids=["odd_spatial", "vec"])
+def test_wide_spmm_layer_padded_rows_and_residual(oracle, hw):
+    """The executor's pointwise step on a wide matrix (channel passes): padded
+    rows truncated, the clamp then the residual applied once, by the last pass."""
+    import torch
+
+    H, W = hw
+    rows, K, B, bh = 10, 1700, 2, 4
+    rng = np.random.default_rng(9)
+    dense = (rng.standard_normal((rows, K)) * 0.1).astype(np.float32)
+    dense[rng.random((rows, K)) < 0.9] = 0
+    pad = (-rows) % bh
+    m = sp.encode_bcsr(np.vstack([dense, np.zeros((pad, K), np.float32)]), bh)
+    act = rng.uniform(-1, 1, (B, K, H, W)).astype(np.float32)
+    bias = rng.uniform(-1, 1, rows).astype(np.float32)
+    res = rng.uniform(-1, 1, (B, rows, H, W)).astype(np.float32)
+    want = oracle.spmm(m, act, np.r_[bias, np.zeros(pad, np.float32)], RELU6)[:, :rows].reshape(B, rows, H, W)
+    dw = sp.DeviceBcsr(m)
+    o = torch.full((B, rows, H, W), float("nan"), device="cuda")
+    sp.spmm_layer(dw, torch.from_numpy(act).cuda(), torch.from_numpy(bias).cuda(), RELU6, o,
+                  residual=torch.from_numpy(res).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o.cpu().numpy()), bits((want + res).astype(np.float32)))
