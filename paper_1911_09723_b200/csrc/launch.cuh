@@ -36,10 +36,10 @@ inline long long geometry_env_key() {
     return key;
 }
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                  cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES>;
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -74,6 +74,15 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC>
 int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                cudaStream_t st) {
+    if (a.acc_in || a.K_img != a.K) {
+        // Channel passes (spcv_cu.cu: pack_passes) are packed with one layout,
+        // so the continuing-sum instantiations exist only for it.
+        if constexpr (STEPS == 4 && LPR == (BH == 4 ? 4 : 2) && NF == (BH == 4 ? 2 : 4))
+            return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true, true>(a, w, ntiles, sms, st)
+                              : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false, true>(a, w, ntiles, sms, st);
+        else
+            return fail(SPCV_ERR_UNSUPPORTED, "spmm: channel pass with an unexpected layout");
+    }
     return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true>(a, w, ntiles, sms, st)
                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
 }

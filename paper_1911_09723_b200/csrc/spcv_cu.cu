@@ -155,6 +155,10 @@ namespace {
 // Input channels per pass when K is too wide for one [K][T] tile.
 constexpr int kPassChannels = 1024;
 
+int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t row_ptr_len,
+              const uint32_t* col_idx, size_t nblocks, const float* values, size_t nvalues,
+              spcv_cu_weights** out, bool pass_part);
+
 // A matrix too wide for one shared-memory tile: packed as parts over channel
 // ranges [k0, k0 + kPassChannels), column indices rebased, every block row
 // present in every part (empty where it has no block in the range). The
@@ -184,8 +188,8 @@ int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const 
             rp[r + 1] = static_cast<uint32_t>(ci.size());
         }
         spcv_cu_weights* part = nullptr;
-        rc = spcv_cu_pack(rows, static_cast<int>(k1) - k0, block_h, rp.data(), rp.size(), ci.data(), ci.size(),
-                          va.data(), va.size(), &part);
+        rc = pack_impl(rows, static_cast<int>(k1) - k0, block_h, rp.data(), rp.size(), ci.data(), ci.size(),
+                       va.data(), va.size(), &part, true);
         if (rc == SPCV_OK) {
             part->jit_eligible = false;  // passes run the tile kernel (it continues sums)
             w->parts.push_back(part);
@@ -223,6 +227,14 @@ int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const 
 extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row_ptr,
                             size_t row_ptr_len, const uint32_t* col_idx, size_t nblocks,
                             const float* values, size_t nvalues, spcv_cu_weights** out) {
+    return pack_impl(rows, cols, block_h, row_ptr, row_ptr_len, col_idx, nblocks, values, nvalues, out, false);
+}
+
+namespace {
+
+int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t row_ptr_len,
+              const uint32_t* col_idx, size_t nblocks, const float* values, size_t nvalues,
+              spcv_cu_weights** out, bool pass_part) {
     g_last_error.clear();
     if (!out) return fail(SPCV_ERR_INVALID, "spcv_cu_pack: out is null");
     *out = nullptr;
@@ -259,7 +271,9 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
         }
     }
 
-    const Layout lay = choose_layout(cols, rows, block_h);
+    // channel-pass parts: the one layout launch.cuh instantiates for them
+    const Layout lay = pass_part ? (block_h == 4 ? Layout{4, 2, 32} : Layout{2, 4, 32})
+                                 : choose_layout(cols, rows, block_h);
     if (lay.LPR == 0 || cols >= 0xFFFF) return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out);
     const int G = 32 / lay.LPR;
     const int T = lay.T;
@@ -281,6 +295,7 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     int steps_fast = short_rows ? 2 : 4;
     if (const char* e = std::getenv("SPCV_STEPS"))
         if (std::atoi(e) == 2 || std::atoi(e) == 4) steps_strict = steps_fast = std::atoi(e);
+    if (pass_part) steps_strict = steps_fast = 4;
 
     // paper-format streams
     std::vector<uint32_t> nnz(brows), delta(nblocks);
@@ -441,6 +456,8 @@ extern "C" int spcv_cu_pack(int rows, int cols, int block_h, const uint32_t* row
     *out = w;
     return SPCV_OK;
 }
+
+}  // namespace
 
 extern "C" int spcv_cu_unpack(const spcv_cu_weights* w, uint32_t* row_ptr, uint32_t* col_idx,
                               float* values) {

@@ -198,7 +198,10 @@ __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a
 #endif
 constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of their FMAs
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES = false>
+// ACC: a channel pass — activations of K_img channels per image, and (after
+// the first pass) accumulators starting at acc_in. A separate instantiation,
+// so the single-pass kernels carry none of its code.
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES = false, bool ACC = false>
 struct Exec {
     static constexpr int G = 32 / LPR;
     static constexpr int T = LPR * NF * 4;
@@ -324,9 +327,11 @@ struct Exec {
         if ((cur.ix[0] & kHeaderHi) == kHeaderHi) {
             finish(a);
             brow = cur.ix[0] & 0xFFFFu;
-            if (a.acc_in) {  // a later channel pass: continue the previous pass's sums
-                load_acc(a);
-                return;
+            if constexpr (ACC) {  // channel pass: a later one continues the previous pass's sums
+                if (a.acc_in) {
+                    load_acc(a);
+                    return;
+                }
             }
 #pragma unroll
             for (int i = 0; i < BH; ++i) {
@@ -417,10 +422,11 @@ __device__ __forceinline__ Chunk<BH, STEPS> zero_chunk() {
 // Issue the cp.async copies of tile [n0, n0+T) into s_act [K][T] (16 B when
 // VEC, 4 B otherwise; zeros past column N) and write its column offsets.
 // Completion: cp.async.wait_all by the issuing threads, then a CTA barrier.
-template <int T, bool VEC>
+template <int T, bool VEC, bool ACC = false>
 __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long long n0,
                                            const KernelArgs& a, int tid, int nthreads) {
-    const long long KS = static_cast<long long>(a.K_img) * a.S;
+    // image stride: K, or the whole matrix's K for a channel pass
+    const long long KS = static_cast<long long>(ACC ? a.K_img : a.K) * a.S;
     for (int c = tid; c < T; c += nthreads) s_col[c] = col_offset(n0 + c, a);
     if constexpr (VEC) {
         constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
@@ -459,10 +465,10 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
 
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 spmm_bcsr_kernel(const KernelArgs a) {
-    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES>;
+    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
     constexpr int G = E::G;
     constexpr int T = E::T;
     constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
@@ -493,7 +499,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
     for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
         reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
             make_float4(0.f, 0.f, 0.f, 0.f);
-    stage_tile<T, VEC>(s_act, s_col, n0, a, tid, nthreads);
+    stage_tile<T, VEC, ACC>(s_act, s_col, n0, a, tid, nthreads);
 
     const int lane = tid & 31;
     const int warp = tid >> 5;
