@@ -476,6 +476,9 @@ def test_wide_matrices_run_as_channel_passes_bit_exact(oracle, case):
         assert np.array_equal(got.reshape(images, M, -1), ident.astype(np.float32))
     fast = run_device(m, act_, bias, act, strict=False)
     assert np.allclose(fast, want, rtol=1e-4, atol=1e-5)
+    host_out = np.full_like(got, np.nan)  # the host-buffer entry point (chunked H2D|kernel|D2H)
+    sp.spmm_host_batched(sp.DeviceBcsr(m), act_, bias, act_of(act), host_out, sp.MicrokernelConfig(n=bh))
+    assert np.array_equal(bits(host_out), bits(want))
     u = sp.DeviceBcsr(m).unpack()
     assert np.array_equal(np.asarray(u.row_ptr), np.asarray(m.row_ptr))
     assert np.array_equal(np.asarray(u.col_idx), np.asarray(m.col_idx))
