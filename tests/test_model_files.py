@@ -359,3 +359,26 @@ def test_forward_graph_replay_matches_run_network(ref, files, mode):
             plain = m.forward(torch.from_numpy(xh).cuda(), False).cpu().numpy()  # default stream: no graph
             assert np.allclose(got, plain, rtol=1e-5, atol=1e-6), it
     assert len(set(counts)) == 1 and counts[0] > 10, counts
+
+
+@pytest.mark.gpu
+def test_forward_graph_cache_eviction(ref, files):
+    """More distinct (input, logits) pairs than the graph cache holds: entries
+    are evicted and re-captured, every forward stays bit-exact."""
+    import torch
+
+    data = files["ours-mbv1-0.25"]
+    m = sp.DeviceModel(data)
+    L0 = m.layers[0]
+    rng = np.random.default_rng(23)
+    s = torch.cuda.Stream()
+    xs = [rng.uniform(-1, 1, (1, L0["in_h"], L0["in_w"], L0["cin"])).astype(np.float32) for _ in range(6)]
+    want = [ref.run_model(data, x) for x in xs]
+    dev_x = [torch.from_numpy(x).cuda() for x in xs]
+    outs = [torch.empty((1, m.layers[-1]["cout"]), device="cuda") for _ in xs]
+    for rnd in range(3):
+        for x, o, w in zip(dev_x, outs, want):
+            with torch.cuda.stream(s):
+                m.forward(x, True, s, out=o)
+            s.synchronize()
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), w.view(np.uint32)), rnd
