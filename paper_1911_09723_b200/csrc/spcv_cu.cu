@@ -579,10 +579,9 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
     const char* env = std::getenv("SPCV_AUTOTUNE");
     if ((env && std::atoi(env) == 0) || std::getenv("SPCV_TAIL") != nullptr) return -1;
     const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
-    auto* mw = const_cast<spcv_cu_weights*>(w);
     {
-        std::lock_guard<std::mutex> lk(mw->tune_mu);
-        for (const auto& kv : mw->tuned_tail)
+        std::lock_guard<std::mutex> lk(w->tune_mu);
+        for (const auto& kv : w->tuned_tail)
             if (kv.first == key) return kv.second;  // also inside a capture / with a residual
     }
     if (a.acc_in) return -1;  // a later channel pass reads out: not repeatable in place
@@ -620,8 +619,8 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     g_launches.fetch_sub(runs, std::memory_order_relaxed);
-    std::lock_guard<std::mutex> lk(mw->tune_mu);
-    mw->tuned_tail.emplace_back(key, best);
+    std::lock_guard<std::mutex> lk(w->tune_mu);
+    w->tuned_tail.emplace_back(key, best);
     return best;
 }
 

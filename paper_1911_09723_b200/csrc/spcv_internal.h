@@ -85,8 +85,8 @@ struct spcv_cu_weights {
     std::vector<spcv_cu_weights*> parts;
     std::vector<int> part_k0;
     // autotuned tail split per call shape (spcv_cu.cu: tuned_tail)
-    std::mutex tune_mu;
-    std::vector<std::pair<long long, int>> tuned_tail;
+    mutable std::mutex tune_mu;
+    mutable std::vector<std::pair<long long, int>> tuned_tail;
 };
 
 namespace spcv_detail {
