@@ -12,13 +12,7 @@ import os
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("SPCV_CU_LIB") or os.path.join(LIB_DIR, "libspcv_cu.so")
 
-# spcv_status (include/spcv_cu.h)
-OK, ERR_LAYOUT, ERR_SHAPE, ERR_FORMAT, ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = range(7)
-ERR_MODEL_IO, ERR_BAD_MAGIC, ERR_VERSION, ERR_TRUNCATED, ERR_CHECKSUM, ERR_MODEL_FORMAT = range(7, 13)
-LAYOUT_CHW, LAYOUT_HWC = 0, 1
-ACT_NONE, ACT_CLAMP = 0, 1
-MODE_STRICT, MODE_FAST = 0, 1
-KERNEL_TILE, KERNEL_JIT = 0, 1
+from ._abi import *  # noqa: F401,F403  (status codes, layouts, modes)
 
 # Every symbol include/spcv_cu.h declares, with (restype, argtypes).
 _p, _i, _f, _z, _u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t, ctypes.c_uint64

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .spmm import BcsrMatrix, encode_bcsr
+from .bcsr import BcsrMatrix, encode_bcsr
 from .workloads import Layer as WLayer
 from .workloads import make_layer_data
 
@@ -212,7 +212,7 @@ def serialize(net: Network) -> bytes:
 def densify(net: Network) -> Network:
     """densify (netdef.cpp:417-431): every sparse 1x1 layer stored dense (the
     logical rows of the decoded matrix), for the effective-vs-dense comparison."""
-    from .spmm import decode_bcsr
+    from .bcsr import decode_bcsr
 
     layers = []
     for L in net.layers:

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .spmm import Activation, BcsrMatrix, encode_bcsr
+from .bcsr import Activation, BcsrMatrix, encode_bcsr  # pure numpy: no CUDA library load
 
 RELU = ("clamp", 0.0, float("inf"))
 RELU6 = ("clamp", 0.0, 6.0)
