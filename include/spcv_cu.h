@@ -128,7 +128,36 @@ int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act, int act_l
                            int out_layout, int out_c, int out_h, int out_w, int cfg_m, int cfg_n,
                            int mode);
 
-/* The network executor's pointwise step (run_network, netdef.cpp:494-512) on
+/* The reference call shape in one call: spmm_into(const BcsrMatrix&, act,
+ * bias, fused, out, cfg) (kernels.hpp:45-46) with the matrix as host BCSR
+ * arrays (sparse.hpp:65-79) and HOST tensors. Arguments are checked first, in
+ * the reference order (as spcv_cu_spmm_into), before the matrix is read; the
+ * matrix is then validated (SPCV_ERR_FORMAT) and packed ONCE per distinct
+ * content and device: later calls with the same arrays find it in an LRU
+ * cache (verified byte for byte; SPCV_WEIGHT_CACHE_MB bounds the cache, 256 by
+ * default), so a caller looping spmm_into over layers and images never
+ * repacks or recompiles. Replaces: spmm_into (kernels.cpp:304-334) as the
+ * reference's callers use it (run_network netdef.cpp:497, bench_layers
+ * bench.cpp:209, run_verify bench.cpp:365). */
+int spcv_cu_spmm_bcsr_into_host(int rows, int cols, int block_h, const uint32_t* row_ptr,
+                                size_t row_ptr_len, const uint32_t* col_idx, size_t nblocks,
+                                const float* values, size_t nvalues, const float* act, int act_layout,
+                                int images, int act_c, int act_h, int act_w, const float* bias,
+                                size_t bias_len, int act_kind, float lo, float hi, float* out,
+                                int out_layout, int out_c, int out_h, int out_w, int cfg_m, int cfg_n,
+                                int mode);
+
+/* Drop every matrix cached by spcv_cu_spmm_bcsr_into_host. */
+void spcv_cu_weight_cache_clear(void);
+
+/* Cache counters (any pointer may be NULL): cached matrices, hits and misses
+ * of spcv_cu_spmm_bcsr_into_host, NVRTC compiles of weight-specialised
+ * kernels and how many of those were served from the on-disk cubin cache
+ * ($SPCV_JIT_CACHE_DIR or ~/.cache/spcv_b200/jit; SPCV_JIT_CACHE=0 disables). */
+int spcv_cu_cache_stats(size_t* entries, uint64_t* hits, uint64_t* misses, uint64_t* jit_compiles,
+                        uint64_t* jit_disk_hits);
+
+/* The network executor's pointwise step/* The network executor's pointwise step (run_network, netdef.cpp:494-512) on
  * device tensors, fused: weights may carry padded rows (w.rows > out_c, up to
  * block_h-1 extra rows; they are computed with bias 0 and never stored, i.e.
  * the "run wide, keep the logical prefix" of netdef.cpp:496-505), and an

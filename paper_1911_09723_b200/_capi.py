@@ -25,6 +25,9 @@ SIGNATURES = {
     "spcv_cu_weights_kernel": (_i, [_p, _i, _p]),
     "spcv_cu_spmm_into": (_i, _SPMM_ARGS + [_p]),
     "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
+    "spcv_cu_spmm_bcsr_into_host": (_i, [_i, _i, _i, _p, _z, _p, _z, _p, _z] + _SPMM_ARGS[1:]),
+    "spcv_cu_weight_cache_clear": (None, []),
+    "spcv_cu_cache_stats": (_i, [_p, _p, _p, _p, _p]),
     "spcv_cu_spmm_layer": (_i, [_p, _p, _i, _i, _i, _i, _p, _z, _i, _f, _f, _p, _p, _i, _i, _p]),
     "spcv_cu_dense_gemm_into": (_i, [_p, _i, _i] + _SPMM_ARGS[1:17] + [_i, _p]),
     "spcv_cu_model_parse": (_i, [_p, _z, _p]),
@@ -64,3 +67,12 @@ def last_error() -> str:
 
 def launch_count() -> int:
     return int(lib.spcv_cu_launch_count())
+
+
+def cache_stats() -> dict:
+    """spcv_cu_cache_stats: packed-weight cache and JIT compile counters."""
+    n = ctypes.c_size_t()
+    h, m, jc, jd = (ctypes.c_uint64() for _ in range(4))
+    lib.spcv_cu_cache_stats(ctypes.byref(n), ctypes.byref(h), ctypes.byref(m), ctypes.byref(jc), ctypes.byref(jd))
+    return {"entries": n.value, "hits": h.value, "misses": m.value, "jit_compiles": jc.value,
+            "jit_disk_hits": jd.value}

@@ -29,8 +29,11 @@
 // netdef.cpp:496-505) are not generated. Requires S % 4 == 0 and 16 B aligned
 // activations (key.vec); other shapes use the tile kernel.
 #include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -57,10 +60,7 @@ int rows_max(int warps, int cpl) {
     return std::max(8, std::min(kRowsMax / cpl, (regs - 48) / cpl));
 }
 
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::atoi(e) : dflt;
-}
+int knob(int v, int dflt) { return v > 0 ? v : dflt; }
 
 // f32 bit pattern duplicated into both halves of a .b64 (f32x2 broadcast).
 std::string imm2(float v) {
@@ -83,10 +83,10 @@ int row_nnz(const uint32_t* row_ptr, int BH, int r) {
 
 // Cut rows [0, m_out) into segments (contiguous rows, cost <= budget, at most
 // kRowsMax rows) and share `sms` CTAs out in proportion to their cost.
-bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key,
+bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& key, const Knobs& kn,
                    std::vector<Segment>& segs) {
-    const int budget = env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr);
-    const int max_segs = std::min(env_int("SPCV_JIT_MAX_SEGS", kJitMaxSegs), key.sms);
+    const int budget = knob(kn.jit_seg_instr, kJitSegInstr);
+    const int max_segs = std::min(knob(kn.jit_max_segs, kJitMaxSegs), key.sms);
     const int per_weight = key.strict ? 2 : 1;
     const int nkc = (K + kKC - 1) / kKC;
     const long long fixed = static_cast<long long>(nkc) * 24 + K;  // copies, waits, LDS.64
@@ -135,7 +135,7 @@ bool plan_segments(int M, int K, int BH, const uint32_t* row_ptr, const JitKey& 
 }
 
 std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint32_t* col_idx,
-                       const float* values, const JitKey& key, const std::vector<Segment>& segs) {
+                       const float* values, const JitKey& key, const Knobs& kn, const std::vector<Segment>& segs) {
     const int nkc = (K + kKC - 1) / kKC;
     const int C = key.cpl;             // columns per lane: 2 (f32x2) or 1 (scalar)
     const int kCols = 32 * C;          // columns per warp group
@@ -174,7 +174,7 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
                 any = true;
             }
     }
-    if (env_int("SPCV_JIT_INTERLEAVE", 1) == 0) {
+    if (kn.jit_interleave == 0) {
         seg_of.clear();
         rank_of.clear();
         for (size_t s = 0; s < segs.size(); ++s)
@@ -436,14 +436,13 @@ std::string gen_direct(int M, int K, int BH, const uint32_t* row_ptr, const uint
 // Which generator serves (matrix, key): direct for small K within the code
 // budget, else the k-major segmented kernel when the layout allows it.
 enum class JitKind { kNone, kDirect, kKMajor };
-JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key,
+JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key, const Knobs& kn,
                     std::vector<Segment>& segs) {
     // fast mode (1 FFMA per weight) affords the direct variant up to K = 128
     // (measured: MBv1 pw3 in the full step 2.387 -> 2.326 ms); strict keeps
     // K <= 64 there (k-major is faster for pw3 strict)
-    const int direct_maxk = env_int("SPCV_JIT_DIRECT_MAXK", key.strict ? kJitDirectMaxK : 2 * kJitDirectMaxK);
-    if (K <= direct_maxk &&
-        direct_instr(M, K, BH, row_ptr, key) <= env_int("SPCV_JIT_SEG_INSTR", kJitSegInstr))
+    const int direct_maxk = knob(kn.jit_direct_maxk, key.strict ? kJitDirectMaxK : 2 * kJitDirectMaxK);
+    if (K <= direct_maxk && direct_instr(M, K, BH, row_ptr, key) <= knob(kn.jit_seg_instr, kJitSegInstr))
         return JitKind::kDirect;
     if (!key.vec || key.dw) return JitKind::kNone;
     // k-major: 2 columns per lane (f32x2), or 1 column per lane (scalar, twice
@@ -454,8 +453,8 @@ JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key,
     k2.cpl = 2;
     k1.cpl = 1;
     std::vector<Segment> s2, s1;
-    const bool ok2 = plan_segments(M, K, BH, row_ptr, k2, s2);
-    const bool ok1 = plan_segments(M, K, BH, row_ptr, k1, s1);
+    const bool ok2 = plan_segments(M, K, BH, row_ptr, k2, kn, s2);
+    const bool ok1 = plan_segments(M, K, BH, row_ptr, k1, kn, s1);
     if (ok1 && s1.size() == 1 && (!ok2 || s2.size() > 1)) {
         segs = s1;  // a single segment reads the activations once
         key.cpl = 1;
@@ -471,21 +470,105 @@ JitKind choose_kind(int M, int K, int BH, const uint32_t* row_ptr, JitKey& key,
 
 std::mutex g_jit_mu;
 
-}  // namespace
+// On-disk cubin cache: NVRTC output keyed by a 128-bit hash of the generated
+// source (which spells out the matrix, the call shape and the geometry), the
+// compile options and the NVRTC version, so a serving process never compiles
+// a (matrix, shape) it has compiled before. $SPCV_JIT_CACHE_DIR, else
+// $XDG_CACHE_HOME/spcv_b200/jit, else ~/.cache/spcv_b200/jit; SPCV_JIT_CACHE=0
+// disables it. Writes are atomic (temporary file + rename); a file that does
+// not load is ignored and replaced.
+std::string cache_dir() {
+    static const std::string dir = [] {
+        const char* off = std::getenv("SPCV_JIT_CACHE");
+        if (off && std::atoi(off) == 0) return std::string();
+        if (const char* d = std::getenv("SPCV_JIT_CACHE_DIR")) return std::string(d);
+        if (const char* x = std::getenv("XDG_CACHE_HOME")) return std::string(x) + "/spcv_b200/jit";
+        if (const char* h = std::getenv("HOME")) return std::string(h) + "/.cache/spcv_b200/jit";
+        return std::string();
+    }();
+    return dir;
+}
 
-namespace spcv_detail {
+std::string cache_name(const std::string& src, const std::vector<const char*>& opts) {
+    uint64_t a = 0xcbf29ce484222325ull, b = 0x84222325cbf29ce4ull;  // FNV-1a / a second multiplier
+    auto mix = [&](const char* p, size_t n) {
+        for (size_t i = 0; i < n; ++i) {
+            a = (a ^ static_cast<unsigned char>(p[i])) * 0x100000001b3ull;
+            b = (b ^ static_cast<unsigned char>(p[i])) * 0x9E3779B97F4A7C15ull;
+            b ^= b >> 29;
+        }
+    };
+    int major = 0, minor = 0;
+    nvrtcVersion(&major, &minor);
+    const std::string ver = std::to_string(major) + "." + std::to_string(minor);
+    mix(ver.data(), ver.size());
+    for (const char* o : opts) mix(o, std::strlen(o) + 1);
+    mix(src.data(), src.size());
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%016llx%016llx.cubin", static_cast<unsigned long long>(a),
+                  static_cast<unsigned long long>(b));
+    return buf;
+}
 
-// NVRTC: source -> sm_100a cubin. No device needed.
-int jit_compile(const std::string& src, std::vector<char>& cubin) {
-    nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, src.c_str(), "spcv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
-        return fail(SPCV_ERR_UNSUPPORTED, "jit: nvrtcCreateProgram failed");
-    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false"};
+bool cache_read(const std::string& path, std::vector<char>& out) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    bool ok = n > 0;
+    if (ok) {
+        out.resize(static_cast<size_t>(n));
+        ok = std::fread(out.data(), 1, out.size(), f) == out.size();
+    }
+    std::fclose(f);
+    return ok;
+}
+
+void cache_write(const std::string& dir, const std::string& name, const std::vector<char>& cubin) {
+    std::string acc;  // mkdir -p
+    for (size_t i = 0; i <= dir.size(); ++i) {
+        if (i == dir.size() || dir[i] == '/') {
+            if (!acc.empty()) mkdir(acc.c_str(), 0755);
+        }
+        if (i < dir.size()) acc += dir[i];
+    }
+    const std::string tmp = dir + "/." + name + "." + std::to_string(getpid());
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    std::fclose(f);
+    if (!ok || std::rename(tmp.c_str(), (dir + "/" + name).c_str()) != 0) std::remove(tmp.c_str());
+}
+
+std::vector<const char*> nvrtc_options() {
     static const std::string maxrreg = [] {
         const char* e = std::getenv("SPCV_JIT_MAXRREG");  // tuning knob (occupancy experiments)
         return e ? std::string("--maxrregcount=") + e : std::string();
     }();
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false"};
     if (!maxrreg.empty()) opts.push_back(maxrreg.c_str());
+    return opts;
+}
+
+}  // namespace
+
+namespace spcv_detail {
+
+std::atomic<uint64_t> g_jit_compiles{0}, g_jit_cache_hits{0};
+
+// NVRTC: source -> sm_100a cubin. No device needed.
+int jit_compile(const std::string& src, std::vector<char>& cubin) {
+    const std::vector<const char*> opts = nvrtc_options();
+    const std::string dir = cache_dir();
+    const std::string name = dir.empty() ? std::string() : cache_name(src, opts);
+    if (!dir.empty() && cache_read(dir + "/" + name, cubin)) {
+        g_jit_cache_hits.fetch_add(1, std::memory_order_relaxed);
+        return SPCV_OK;
+    }
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "spcv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        return fail(SPCV_ERR_UNSUPPORTED, "jit: nvrtcCreateProgram failed");
     if (nvrtcCompileProgram(prog, static_cast<int>(opts.size()), opts.data()) != NVRTC_SUCCESS) {
         size_t n = 0;
         nvrtcGetProgramLogSize(prog, &n);
@@ -499,28 +582,50 @@ int jit_compile(const std::string& src, std::vector<char>& cubin) {
     cubin.resize(n);
     nvrtcGetCUBIN(prog, cubin.data());
     nvrtcDestroyProgram(&prog);
+    g_jit_compiles.fetch_add(1, std::memory_order_relaxed);
+    if (!dir.empty()) cache_write(dir, name, cubin);
     return SPCV_OK;
 }
 
-const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
+const JitVariant* jit_plan(const spcv_cu_weights* w, const JitKey& key) {
+    if (!w || !w->jit_eligible) return nullptr;
     std::lock_guard<std::mutex> lk(g_jit_mu);
     for (const JitVariant& v : w->jit)
-        if (v.key == key) return v.fn ? &v : nullptr;
+        if (v.key == key) return v.eligible ? &v : nullptr;
     w->jit.emplace_back();
     JitVariant& v = w->jit.back();
     v.key = key;
     std::vector<Segment> segs;
     JitKey gk = key;  // plus the generator's choices (columns per lane)
-    const JitKind kind = choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), gk, segs);
+    const JitKind kind = choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), gk, w->knobs, segs);
     if (kind == JitKind::kNone) return nullptr;  // the tile kernel runs
+    v.eligible = true;
     v.direct = kind == JitKind::kDirect;
     v.cpl = gk.cpl;
+    v.segments = static_cast<int>(segs.size());
+    return &v;
+}
+
+const JitVariant* jit_build(const spcv_cu_weights* w, const JitVariant* cv) {
+    if (!cv) return nullptr;
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    // the variant lives in w->jit (mutable cache): find the non-const element
+    JitVariant* vp = nullptr;
+    for (JitVariant& x : w->jit)
+        if (&x == cv) vp = &x;
+    if (!vp) return nullptr;
+    JitVariant& v = *vp;
+    if (v.built) return v.fn ? &v : nullptr;
+    v.built = true;
+    std::vector<Segment> segs;
+    JitKey gk = v.key;
+    choose_kind(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), gk, w->knobs, segs);  // same plan
     std::vector<char> cubin;
     const std::string src =
         v.direct ? gen_direct(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
-                              w->h_values.data(), key)
+                              w->h_values.data(), v.key)
                  : gen_source(w->rows, w->cols, w->block_h, w->h_row_ptr.data(), w->h_col_idx.data(),
-                              w->h_values.data(), gk, segs);
+                              w->h_values.data(), gk, w->knobs, segs);
     if (jit_compile(src, cubin) != SPCV_OK) return nullptr;
     cudaError_t e = cudaLibraryLoadData(&v.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
@@ -532,7 +637,7 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
     if (e == cudaSuccess && !v.direct)
         e = cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 jit_smem_bytes(key.warps, key.stages, v.cpl));
+                                 jit_smem_bytes(v.key.warps, v.key.stages, v.cpl));
     if (e != cudaSuccess) {
         cuda_fail(e, "jit: kernel setup");
         cudaLibraryUnload(v.lib);
@@ -540,13 +645,12 @@ const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key) {
         v.fn = nullptr;
         return nullptr;
     }
-    v.segments = static_cast<int>(segs.size());
     return &v;
 }
 
-void jit_geometry(JitKey& key) {
-    key.warps = env_int("SPCV_JIT_WARPS", kJitWarps);
-    key.stages = env_int("SPCV_JIT_STAGES", kJitStages);
+void jit_geometry(JitKey& key, const Knobs& kn) {
+    key.warps = knob(kn.jit_warps, kJitWarps);
+    key.stages = knob(kn.jit_stages, kJitStages);
     if (key.warps < 1 || key.warps > 32) key.warps = kJitWarps;
     if (key.stages < 1 || key.stages > 8) key.stages = kJitStages;
     while (key.stages > 1 && jit_smem_bytes(key.warps, key.stages) > 227 * 1024) --key.stages;
@@ -606,14 +710,15 @@ extern "C" int spcvx_jit_compile(int rows, int cols, int block_h, const uint32_t
     key.m_out = m_out;
     key.vec = true;
     key.sms = sms;
-    spcv_detail::jit_geometry(key);
+    const Knobs kn = Knobs::from_env();
+    spcv_detail::jit_geometry(key, kn);
     std::vector<Segment> segs;
-    const JitKind kind = choose_kind(rows, cols, block_h, row_ptr, key, segs);
+    const JitKind kind = choose_kind(rows, cols, block_h, row_ptr, key, kn, segs);
     if (kind == JitKind::kNone) return SPCV_ERR_UNSUPPORTED;
     if (segments) *segments = kind == JitKind::kDirect ? 0 : static_cast<int>(segs.size());
     const std::string src = kind == JitKind::kDirect
                                 ? gen_direct(rows, cols, block_h, row_ptr, col_idx, values, key)
-                                : gen_source(rows, cols, block_h, row_ptr, col_idx, values, key, segs);
+                                : gen_source(rows, cols, block_h, row_ptr, col_idx, values, key, kn, segs);
     if (src_bytes) *src_bytes = src.size();
     if (src_out && src_cap) {
         const size_t n = std::min(src_cap - 1, src.size());

@@ -26,16 +26,6 @@ struct Geometry {
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref);
 
-// The geometry knobs (SPCV_NWARPS, SPCV_SPLIT, SPCV_TAIL) as one cache-key value.
-inline long long geometry_env_key() {
-    long long key = 0;
-    for (const char* name : {"SPCV_NWARPS", "SPCV_SPLIT", "SPCV_TAIL"}) {
-        const char* e = std::getenv(name);
-        key = key * 64 + (e ? (std::atoi(e) & 31) + 1 : 0);
-    }
-    return key;
-}
-
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                  cudaStream_t st) {
@@ -54,7 +44,7 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     // knobs: cache the last one.
     static thread_local long long key[7] = {-1, -1, -1, -1, -1, -1, -2};
     static thread_local Geometry g;
-    const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, geometry_env_key(), a.tail_pref};
+    const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, w->knobs.geometry_key(), a.tail_pref};
     if (!std::equal(k, k + 7, key)) {
         g = geometry(kern, w, ntiles, sms, a.tail_pref);
         std::copy(k, k + 7, key);
@@ -87,61 +77,9 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
 }
 
-// Shared memory of the pipelined kernel with `ns` stages.
-inline size_t pipe_smem_bytes(int K, int M, int T, int ns) {
-    const size_t stage = static_cast<size_t>(K + 1) * T * 4 + static_cast<size_t>(T) * 8;
-    return 2 * spcvk::kPipeMaxStages * 8 + ((static_cast<size_t>(M) * 4 + 127) & ~size_t{127}) +
-           stage * ns;
-}
-
-// Stages of the pipelined kernel that fit (0 when fewer than two do).
-inline int pipe_stages(const spcv_cu_weights* w) {
-    for (int ns = spcvk::kPipeMaxStages; ns >= 2; --ns)
-        if (pipe_smem_bytes(w->cols, w->rows, w->T, ns) <= kSmemLimit) return ns;
-    return 0;
-}
-
-template <int BH, int LPR, int NF, bool STRICT>
-int launch_pipe(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
-                int ns, cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_pipelined<BH, LPR, NF, STRICT>;
-    static std::atomic<uint64_t> configured{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(configured.load() & bit)) {
-        SPCV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kSmemLimit)));
-        configured.fetch_or(bit);
-    }
-    const size_t smem = pipe_smem_bytes(w->cols, w->rows, w->T, ns);
-    const long long grid_x = std::min<long long>(ntiles, sms);
-    dim3 grid(static_cast<unsigned>(grid_x), 1u);
-    kern<<<grid, spcvk::kPipeThreads, smem, st>>>(a, ns, ntiles);
-    SPCV_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return SPCV_OK;
-}
-
 template <int BH, int LPR, int NF, int STEPS>
 int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
              bool strict, bool vec, cudaStream_t st) {
-    // Kernel choice: the one-tile-per-CTA kernel; SPCV_KERNEL=pipe (or
-    // SPCV_PIPELINE=1) selects the bulk-copy pipeline (4-step chunks only).
-    const char* kenv = std::getenv("SPCV_KERNEL");
-    const std::string kind = kenv ? kenv : "";
-    // Pipelined persistent kernel when the tile ring fits >= 2 stages and there
-    // are enough tiles to keep every SM streaming; else one tile per CTA.
-    const int ns = vec ? pipe_stages(w) : 0;
-    const char* env = std::getenv("SPCV_PIPELINE");
-    // Opt-in for now: with 8 consumer warps it trails the tile kernel (profiles/).
-    const bool pipe = ns >= 2 && ((env && std::atoi(env) != 0) || kind == "pipe") && a.acc_in == nullptr &&
-                      a.K_img == a.K;  // channel passes: the tile kernel only
-    if constexpr (STEPS == 4) {
-        if (pipe)
-            return strict ? launch_pipe<BH, LPR, NF, true>(a, w, nt, sms, ns, st)
-                          : launch_pipe<BH, LPR, NF, false>(a, w, nt, sms, ns, st);
-    }
     if (strict)
         return vec ? launch_one<BH, LPR, NF, STEPS, true, true>(a, w, nt, sms, st)
                    : launch_one<BH, LPR, NF, STEPS, true, false>(a, w, nt, sms, st);
@@ -188,10 +126,10 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     g.smem = smem_bytes(w->cols, w->rows, w->T);
     int best = 0, per_sm = 1;
     g.nwarps = 16;
-    const char* env_nw = std::getenv("SPCV_NWARPS");
+    const Knobs& kn = w->knobs;
     for (int nw : {4, 8, 16}) {
         if (nw * 32 > spcvk::kThreads) continue;
-        if (env_nw && std::atoi(env_nw) != nw) continue;
+        if (kn.nwarps && kn.nwarps != nw) continue;
         int ctas = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)
             ctas = 0;
@@ -204,8 +142,8 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     g.split = 1;
     while (g.nwarps * g.split * 2 <= kBins && ntiles * g.split < static_cast<long long>(sms) * per_sm)
         g.split *= 2;
-    if (const char* e = std::getenv("SPCV_SPLIT")) {
-        const int want = std::atoi(e);
+    if (kn.split) {
+        const int want = kn.split;
         if (want >= 1 && g.nwarps * want <= kBins && (want & (want - 1)) == 0) g.split = want;
     }
     // Tail splitting: if the last wave of CTAs is partial, split its tiles
@@ -216,8 +154,7 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     const long long total = ntiles * g.split;
     const long long full_rounds = total / resident;
     const long long left = total - full_rounds * resident;  // CTAs in the partial round
-    const char* env_tail = std::getenv("SPCV_TAIL");
-    if (full_rounds >= 1 && left > 0 && !(env_tail && std::atoi(env_tail) == 0)) {
+    if (full_rounds >= 1 && left > 0 && kn.tail != 0) {
         int ts = 1;
         if (per_sm == 1) {
             // One CTA per SM (K ~ 1024): split the partial round's tiles ts ways
@@ -238,7 +175,7 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
             while (ts < 8 && g.nwarps * g.split * ts * 2 <= kBins && left * ts * 4 < resident * 3) ts *= 2;
         }
         if (tail_pref >= 0) ts = std::max(1, tail_pref);                      // autotuned (spcv_cu.cu)
-        if (env_tail && std::atoi(env_tail) > 1) ts = std::atoi(env_tail);  // tuning aid
+        if (kn.tail > 1) ts = kn.tail;  // tuning aid
         if (ts > 1 && g.nwarps * g.split * ts <= kBins) {
             g.tail_split = ts;
             g.tail_start = ntiles - left / g.split;

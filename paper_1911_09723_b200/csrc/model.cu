@@ -299,6 +299,7 @@ void free_model(spcv_cu_model* m) {
     if (m->pool || !m->graphs.empty()) cudaDeviceSynchronize();  // no forward may still run
     for (auto& g : m->graphs) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.done) cudaEventDestroy(g.done);
         for (float* p : g.ws) cudaFree(p);
     }
     if (m->pool) cudaMemPoolDestroy(m->pool);

@@ -68,17 +68,27 @@ struct spcv_cu_model {
     cudaMemPool_t pool = nullptr;
     // forward() replayed as a CUDA graph per (images, input, logits, mode,
     // stream) for small batches (network.cu)
-    struct GraphEntry {
-        int images = 0, mode = 0, uses = 0;
+    struct GraphKey {
+        int images = 0, mode = 0;
         const float* input = nullptr;
         float* logits = nullptr;
         cudaStream_t stream = nullptr;
+        bool operator==(const GraphKey& o) const {
+            return images == o.images && mode == o.mode && input == o.input && logits == o.logits &&
+                   stream == o.stream;
+        }
+    };
+    struct GraphEntry {
+        GraphKey key;
+        int uses = 0;
         cudaGraphExec_t exec = nullptr;
+        cudaEvent_t done = nullptr;  // recorded after the entry's last forward / replay
         bool failed = false;
         uint64_t launches = 0;
-        std::vector<float*> ws;  // persistent workspace the graph reads and writes
+        std::vector<float*> ws;  // persistent workspace (model pool) the graph reads and writes
     };
     mutable std::mutex graph_mu;
-    mutable std::deque<GraphEntry> graphs;
+    mutable std::deque<GraphEntry> graphs;  // least recently used first
+    mutable std::deque<GraphKey> seen;      // keys seen once (no entry yet), least recent first
 };
 

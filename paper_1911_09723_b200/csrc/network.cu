@@ -726,9 +726,10 @@ int forward_impl(const spcv_cu_model* m, const float* input, int images, float* 
     size_t next = 0;  // persistent workspace: buffers in allocation order
     auto alloc = [&](size_t bytes, float** p) -> int {
         if (ws) {
-            if (next == ws->size()) {
+            if (next == ws->size()) {  // from the model's pool, kept until the entry is evicted
                 float* q = nullptr;
-                SPCV_CUDA(cudaMalloc(reinterpret_cast<void**>(&q), std::max<size_t>(bytes, 4)));
+                SPCV_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&q), std::max<size_t>(bytes, 4),
+                                                  m->pool, st));
                 ws->push_back(q);
             }
             *p = (*ws)[next++];
@@ -846,14 +847,17 @@ int forward_impl(const spcv_cu_model* m, const float* input, int images, float* 
     return rc;
 }
 
-// Replays of a captured forward (serving): a forward issued again with the same
-// (images, input, logits, mode, stream) is captured into a
-// CUDA graph over a persistent workspace and replayed from then on (one graph
-// launch instead of ~30 kernel launches). Only for batches up to
-// SPCV_MODEL_GRAPH_MAX_IMAGES (default 16: the persistent workspace of a
-// cached batch stays allocated until spcv_cu_model_free) and non-default
-// streams; SPCV_MODEL_GRAPH=0 disables it. A failed capture falls back to
-// plain launches for that key.
+// Replays of a captured forward (serving): a forward issued a third time with
+// the same (images, input, logits, mode, stream) replays a CUDA graph captured
+// over a persistent workspace (one graph launch instead of ~30 kernel
+// launches). The first sighting of a key only remembers it (plain launches,
+// pool workspace); the second makes an entry and allocates its persistent
+// workspace from the model's pool; the third captures. At most 4 entries are
+// kept, least recently used evicted: its workspace returns to the pool
+// stream-ordered behind its last replay (an event), with no device-wide sync.
+// Only for batches up to SPCV_MODEL_GRAPH_MAX_IMAGES (default 16) on
+// non-default streams; SPCV_MODEL_GRAPH=0 disables it. A failed capture
+// falls back to plain launches for that key.
 int graph_max_images() {
     static const int v = [] {
         const char* off = std::getenv("SPCV_MODEL_GRAPH");
@@ -891,37 +895,62 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
         return forward_impl(m, input, images, logits, mode, st, nullptr);
 
     std::lock_guard<std::mutex> lk(m->graph_mu);
-    spcv_cu_model::GraphEntry* e = nullptr;
-    for (auto& g : m->graphs)
-        if (g.images == images && g.input == input && g.logits == logits && g.mode == mode && g.stream == st) e = &g;
-    if (!e) {
-        constexpr size_t kMaxGraphs = 4;  // oldest entry evicted (its stream drained first)
-        if (m->graphs.size() == kMaxGraphs) {
-            spcv_cu_model::GraphEntry& old = m->graphs.front();
-            cudaStreamSynchronize(old.stream);
-            if (old.exec) cudaGraphExecDestroy(old.exec);
-            for (float* p : old.ws) cudaFree(p);
-            m->graphs.pop_front();
+    using Entry = spcv_cu_model::GraphEntry;
+    const spcv_cu_model::GraphKey key{images, mode, input, logits, st};
+    auto& graphs = m->graphs;
+    Entry* e = nullptr;
+    for (size_t i = 0; i < graphs.size(); ++i)
+        if (graphs[i].key == key) {  // hit: becomes the most recently used
+            if (i + 1 != graphs.size()) {
+                Entry moved = std::move(graphs[i]);
+                graphs.erase(graphs.begin() + static_cast<long>(i));
+                graphs.push_back(std::move(moved));
+            }
+            e = &graphs.back();
+            break;
         }
-        m->graphs.emplace_back();
-        e = &m->graphs.back();
-        e->images = images;
-        e->input = input;
-        e->logits = logits;
-        e->mode = mode;
-        e->stream = st;
+    if (!e) {
+        // First sighting of a key: plain launches from the pool, only remembered.
+        // An entry (persistent workspace, later a graph) is made on the second.
+        auto it = std::find(m->seen.begin(), m->seen.end(), key);
+        if (it == m->seen.end()) {
+            constexpr size_t kMaxSeen = 16;
+            if (m->seen.size() == kMaxSeen) m->seen.pop_front();
+            m->seen.push_back(key);
+            return forward_impl(m, input, images, logits, mode, st, nullptr);
+        }
+        m->seen.erase(it);
+        constexpr size_t kMaxGraphs = 4;  // least recently used evicted
+        if (graphs.size() == kMaxGraphs) {
+            Entry& old = graphs.front();
+            // its workspace goes back to the pool once its last replay is done:
+            // ordered on this stream behind that replay, no device-wide sync
+            if (old.done) SPCV_CUDA(cudaStreamWaitEvent(st, old.done, 0));
+            for (float* p : old.ws) cudaFreeAsync(p, st);
+            if (old.exec) cudaGraphExecDestroy(old.exec);  // an in-flight replay finishes first
+            if (old.done) cudaEventDestroy(old.done);
+            graphs.pop_front();
+        }
+        graphs.emplace_back();
+        e = &graphs.back();
+        e->key = key;
+        SPCV_CUDA(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
     }
+    auto mark_done = [&](int rc) {
+        if (rc == SPCV_OK && e->done) cudaEventRecord(e->done, st);
+        return rc;
+    };
     if (e->exec) {
         SPCV_CUDA(cudaGraphLaunch(e->exec, st));
         g_launches.fetch_add(e->launches, std::memory_order_relaxed);
-        return SPCV_OK;
+        return mark_done(SPCV_OK);
     }
     if (e->failed || e->uses < 1) {
-        // 1st call: plain launches (kernels compiled and configured, the
-        // persistent workspace allocated); from the 2nd on: the graph
+        // 2nd sighting: plain launches into the persistent workspace (kernels
+        // compiled and configured, workspace allocated); from the 3rd on: the graph
         const int rc = forward_impl(m, input, images, logits, mode, st, e->failed ? nullptr : &e->ws);
         if (rc == SPCV_OK) ++e->uses;
-        return rc;
+        return mark_done(rc);
     }
     const uint64_t n0 = g_launches.load();
     cudaGraph_t graph = nullptr;
@@ -940,10 +969,10 @@ extern "C" int spcv_cu_model_forward(const spcv_cu_model* m, const float* input,
     e->launches = g_launches.load() - n0;
     if (rc != SPCV_OK || !e->exec) {
         e->failed = true;
-        return forward_impl(m, input, images, logits, mode, st, nullptr);
+        return mark_done(forward_impl(m, input, images, logits, mode, st, nullptr));
     }
     g_launches.fetch_sub(e->launches, std::memory_order_relaxed);  // recorded, not launched
     SPCV_CUDA(cudaGraphLaunch(e->exec, st));
     g_launches.fetch_add(e->launches, std::memory_order_relaxed);
-    return SPCV_OK;
+    return mark_done(SPCV_OK);
 }

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <list>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -40,6 +42,31 @@ int cuda_fail(cudaError_t e, const char* what) {
 }  // namespace spcv_detail
 
 using namespace spcv_detail;
+
+Knobs Knobs::from_env() {
+    auto get = [](const char* name, long long dflt) -> long long {
+        const char* e = std::getenv(name);
+        return e ? std::atoll(e) : dflt;
+    };
+    Knobs k;
+    k.steps = static_cast<int>(get("SPCV_STEPS", 0));
+    k.nf = static_cast<int>(get("SPCV_NF", 0));
+    k.tile_t = static_cast<int>(get("SPCV_TILE_T", 0));
+    k.nwarps = static_cast<int>(get("SPCV_NWARPS", 0)) & 31;
+    k.split = static_cast<int>(get("SPCV_SPLIT", 0)) & 31;
+    k.tail = static_cast<int>(std::min<long long>(get("SPCV_TAIL", -1), 31));
+    k.autotune = get("SPCV_AUTOTUNE", 1) != 0;
+    k.jit = get("SPCV_JIT", 1) != 0;
+    k.fuse_dw = get("SPCV_FUSE_DW", 0) != 0;
+    k.kmajor_min_cols = get("SPCV_JIT_KMAJOR_MIN_COLS", -1);
+    k.jit_warps = static_cast<int>(get("SPCV_JIT_WARPS", 0));
+    k.jit_stages = static_cast<int>(get("SPCV_JIT_STAGES", 0));
+    k.jit_seg_instr = static_cast<int>(get("SPCV_JIT_SEG_INSTR", 0));
+    k.jit_max_segs = static_cast<int>(get("SPCV_JIT_MAX_SEGS", 0));
+    k.jit_direct_maxk = static_cast<int>(get("SPCV_JIT_DIRECT_MAXK", 0));
+    k.jit_interleave = static_cast<int>(get("SPCV_JIT_INTERLEAVE", 1));
+    return k;
+}
 
 namespace spcvk {
 
@@ -84,15 +111,14 @@ struct Layout {
 // the shared-memory pipe). The widest tile T whose shared-memory footprint
 // leaves room for two CTAs per SM wins, else the widest that fits one CTA.
 // SPCV_NF=2|4 and SPCV_TILE_T=32|64|128 override (tuning aids).
-Layout choose_layout(int K, int M, int block_h) {
+Layout choose_layout(int K, int M, int block_h, const Knobs& kn) {
     int NF = (block_h == 4 || M <= 96) ? 2 : 4;
-    if (const char* e = std::getenv("SPCV_NF"))  // tuning aid: 2 or 4 float4 quads per lane
-        if (block_h != 4 && (std::atoi(e) == 2 || std::atoi(e) == 4)) NF = std::atoi(e);
+    if (block_h != 4 && (kn.nf == 2 || kn.nf == 4)) NF = kn.nf;  // tuning aid
     const int lprs_nf4[3] = {8, 4, 2};
     const int lprs_nf2[3] = {16, 8, 4};
     const int* lprs = NF == 2 ? lprs_nf2 : lprs_nf4;
-    if (const char* e = std::getenv("SPCV_TILE_T")) {
-        const int want = std::atoi(e);
+    if (kn.tile_t) {
+        const int want = kn.tile_t;
         for (int i = 0; i < 3; ++i)
             if (lprs[i] * NF * 4 == want && smem_bytes(K, M, want) <= kSmemLimit)
                 return {lprs[i], NF, want};
@@ -173,6 +199,7 @@ int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const 
     w->block_h = block_h;
     w->brows = brows;
     w->nblocks = nblocks;
+    w->knobs = Knobs::from_env();
     cudaGetDevice(&w->device);
     int rc = SPCV_OK;
     for (int k0 = 0; k0 < cols && rc == SPCV_OK; k0 += kPassChannels) {
@@ -272,8 +299,9 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     }
 
     // channel-pass parts: the one layout launch.cuh instantiates for them
+    const Knobs kn = Knobs::from_env();
     const Layout lay = pass_part ? (block_h == 4 ? Layout{4, 2, 32} : Layout{2, 4, 32})
-                                 : choose_layout(cols, rows, block_h);
+                                 : choose_layout(cols, rows, block_h, kn);
     if (lay.LPR == 0 || cols >= 0xFFFF) return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out);
     const int G = 32 / lay.LPR;
     const int T = lay.T;
@@ -293,8 +321,7 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     const bool small_square = block_h == 1 && rows <= 512 && rows >= cols;
     int steps_strict = (short_rows || small_square) ? 2 : 4;
     int steps_fast = short_rows ? 2 : 4;
-    if (const char* e = std::getenv("SPCV_STEPS"))
-        if (std::atoi(e) == 2 || std::atoi(e) == 4) steps_strict = steps_fast = std::atoi(e);
+    if (kn.steps == 2 || kn.steps == 4) steps_strict = steps_fast = kn.steps;
     if (pass_part) steps_strict = steps_fast = 4;
 
     // paper-format streams
@@ -427,13 +454,12 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     w->T = T;
     w->nblocks = nblocks;
     w->nchunks = bs.nchunks;
+    w->knobs = kn;
     cudaGetDevice(&w->device);
     // Small-K matrices also get a weight-specialised kernel (jit.cu), compiled
     // on first use. SPCV_JIT=0 disables it, so the tile kernel runs everywhere.
     {
-        const char* e = std::getenv("SPCV_JIT");
-        const bool off = e && std::atoi(e) == 0;
-        w->jit_eligible = !off && nvalues <= kJitMaxWeights;
+        w->jit_eligible = kn.jit && nvalues <= kJitMaxWeights;
         if (w->jit_eligible) {
             w->h_row_ptr.assign(row_ptr, row_ptr + brows + 1);
             w->h_col_idx.assign(col_idx, col_idx + nblocks);
@@ -522,7 +548,7 @@ extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel)
         key.vec = true;
         key.m_out = w->rows;
         key.sms = props_for(w->device).sms;
-        jit_geometry(key);
+        jit_geometry(key, w->knobs);
         if (jit_prepare(w, key)) *kernel = SPCV_KERNEL_JIT;
         cudaSetDevice(prev);
     }
@@ -576,8 +602,7 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
 template <typename Run>
 int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, bool strict, bool vec,
                cudaStream_t st, Run&& run) {
-    const char* env = std::getenv("SPCV_AUTOTUNE");
-    if ((env && std::atoi(env) == 0) || std::getenv("SPCV_TAIL") != nullptr) return -1;
+    if (!w->knobs.autotune || w->knobs.tail >= 0) return -1;
     const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
     {
         std::lock_guard<std::mutex> lk(w->tune_mu);
@@ -686,7 +711,6 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                      (reinterpret_cast<uintptr_t>(acc_in) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
     if (w->jit_eligible) {
-        // const_cast: the compiled kernel is a cache inside the weights object
         // A failed compile (recorded, never retried) falls back to the tile kernel.
         JitKey key;
         key.strict = strict;
@@ -698,21 +722,19 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                   reinterpret_cast<uintptr_t>(residual) % 8 == 0;
         key.m_out = a.M_out;
         key.sms = sms;
-        jit_geometry(key);
+        jit_geometry(key, w->knobs);
         // The k-major variant is persistent (one CTA per SM, 32 or 64 columns
         // per warp group, each segment on its share of the SMs): with fewer
         // column groups than its warps the tile kernel's finer tiles win
         // (measured: c1, 784 columns, 24 vs 17 us; MBv2 384->64 @14x14 x128,
-        // 25088 columns in 2 segments, 53 vs 38 us).
-        static const long long min_cols_env = [] {
-            const char* e = std::getenv("SPCV_JIT_KMAJOR_MIN_COLS");
-            return e ? std::atoll(e) : -1LL;
-        }();
-        if (const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key)) {
-            const long long min_cols =
-                min_cols_env >= 0 ? min_cols_env
-                                  : 32LL * v->cpl * sms * key.warps / std::max(1, v->segments);
-            if (v->direct || N >= min_cols) return jit_launch(v, a, st);
+        // 25088 columns in 2 segments, 53 vs 38 us). Decided from the plan, so
+        // a variant that would not run is never compiled.
+        if (const JitVariant* p = jit_plan(w, key)) {
+            const long long min_cols = w->knobs.kmajor_min_cols >= 0
+                                           ? w->knobs.kmajor_min_cols
+                                           : 32LL * p->cpl * sms * key.warps / std::max(1, p->segments);
+            if (p->direct || N >= min_cols)
+                if (const JitVariant* v = jit_build(w, p)) return jit_launch(v, a, st);
         }
     }
     auto run = [&](const spcvk::KernelArgs& args) {
@@ -759,6 +781,39 @@ size_t host_chunk_bytes() {
         return v > 0 ? static_cast<size_t>(v) << 20 : kHostChunkBytes;
     }();
     return b;
+}
+
+bool host_ramp() {
+    static const bool r = [] {
+        const char* e = std::getenv("SPCV_HOST_RAMP");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return r;
+}
+
+// Image chunks of the host-buffer entry point: chunk = as many images as fit
+// `budget` bytes (at least 1). With the ramp, the schedule starts and ends
+// with 1/8, 1/4, 1/2 of a chunk (the first kernel starts early, the last
+// download is short) when a chunk is large enough for those to be real
+// fractions. The sizes are positive and always sum to `images`.
+std::vector<int> host_chunks(int images, size_t per_image, size_t budget, bool ramp) {
+    std::vector<int> sizes;
+    if (images <= 0) return sizes;
+    const int chunk = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(static_cast<size_t>(images), budget / std::max<size_t>(per_image, 1))));
+    std::vector<int> head;
+    if (ramp && chunk >= 8 && images >= 4 * chunk)
+        for (int f : {8, 4, 2}) head.push_back(chunk / f);
+    int left = images;
+    for (int n : head) left -= 2 * n;  // ramp-up and the mirrored ramp-down
+    sizes = head;
+    while (left > 0) {
+        const int n = std::min(chunk, left);
+        sizes.push_back(n);
+        left -= n;
+    }
+    sizes.insert(sizes.end(), head.rbegin(), head.rend());
+    return sizes;
 }
 
 }  // namespace
@@ -815,8 +870,7 @@ int spmm_dw_fused(const spcv_cu_weights* w, const JitDwArgs& dw, int dw_stride, 
     // on MBv1-1.0 (dw1+pw1 507 vs 550 us, dw2+pw2 392 vs 323 us): the fused
     // producer recomputes each depthwise output per 1x1 column thread and
     // becomes issue-bound.
-    const char* e = std::getenv("SPCV_FUSE_DW");
-    if (!e || std::atoi(e) == 0) return SPCV_ERR_UNSUPPORTED;
+    if (!w->knobs.fuse_dw) return SPCV_ERR_UNSUPPORTED;
     const long long S = static_cast<long long>(out_h) * out_w;
     const long long N = S * images;
     if (N == 0) return SPCV_OK;
@@ -830,13 +884,13 @@ int spmm_dw_fused(const spcv_cu_weights* w, const JitDwArgs& dw, int dw_stride, 
     key.res = residual != nullptr;
     key.m_out = out_c;
     key.sms = props_for(dev).sms;
-    jit_geometry(key);
+    jit_geometry(key, w->knobs);
     key.dw = true;
     key.dw_clamp = dw_clamp;
     key.dw_stride = dw_stride;
     key.dw_w = dw_w_host;
     key.dw_b = dw_b_host;
-    const JitVariant* v = jit_prepare(const_cast<spcv_cu_weights*>(w), key);
+    const JitVariant* v = jit_prepare(w, key);
     if (!v || !v->direct) return SPCV_ERR_UNSUPPORTED;
     spcvk::KernelArgs a{};
     a.out = out;
@@ -870,11 +924,25 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
     SPCV_CUDA(cudaGetDevice(&prev));
     SPCV_CUDA(cudaSetDevice(w->device));
     HostScratch& hs = g_scratch;
+    // Every exit after this point goes through done(): all three streams are
+    // drained (no copy may still write the caller's `out` after we return) and
+    // the caller's device is restored.
+    auto done = [&](int code) {
+        for (cudaStream_t s : {hs.h2d, hs.k, hs.d2h})
+            if (s) cudaStreamSynchronize(s);
+        cudaSetDevice(prev);
+        return code;
+    };
+#define SPCV_HOST_CUDA(call)                                        \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return done(cuda_fail(e_, #call));   \
+    } while (0)
     if (hs.device != w->device) {
         hs.release();
-        hs.device = w->device;
         for (cudaStream_t* st : {&hs.h2d, &hs.k, &hs.d2h})
-            SPCV_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+            SPCV_HOST_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+        hs.device = w->device;  // only once every stream exists
     }
     // 16 B-aligned sub-buffers: act | out | bias
     auto up4 = [](size_t n) { return (n + 3) & ~static_cast<size_t>(3); };
@@ -883,72 +951,192 @@ extern "C" int spcv_cu_spmm_into_host(const spcv_cu_weights* w, const float* act
         if (hs.buf) cudaFree(hs.buf);
         hs.buf = nullptr;
         hs.cap = 0;
-        SPCV_CUDA(cudaMalloc(&hs.buf, need * sizeof(float)));
+        SPCV_HOST_CUDA(cudaMalloc(&hs.buf, need * sizeof(float)));
         hs.cap = need;
     }
     float* d_act = hs.buf;
     float* d_out = d_act + up4(n_in);
     float* d_bias = n_bias ? d_out + up4(n_out) : nullptr;
 
-    // Image chunks of ~kHostChunkBytes; each chunk: H2D -> kernel -> D2H.
     const size_t per_image = S * (static_cast<size_t>(act_c) + out_c) * sizeof(float);
-    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(images, host_chunk_bytes() / std::max<size_t>(per_image, 1))));
-    // Chunk schedule: ramp up (1/8, 1/4, 1/2 of a full chunk) so the first
-    // kernel starts early, full chunks in the middle, ramp down at the end so
-    // the last download is short: the pipeline's fill and drain shrink.
-    std::vector<int> sizes;
-    {
-        const bool ramp = std::getenv("SPCV_HOST_RAMP") == nullptr || std::atoi(std::getenv("SPCV_HOST_RAMP")) != 0;
-        int left = images;
-        std::vector<int> tail;
-        if (ramp && images >= 4 * chunk) {
-            for (int f : {8, 4, 2}) {
-                const int n = std::max(1, chunk / f);
-                sizes.push_back(n);
-                tail.push_back(n);
-                left -= 2 * n;
-            }
-        }
-        while (left > 0) {
-            const int n = std::min(chunk, left);
-            sizes.push_back(n);
-            left -= n;
-        }
-        sizes.insert(sizes.end(), tail.rbegin(), tail.rend());  // 1/2, 1/4, 1/8 of a chunk
-    }
+    const std::vector<int> sizes = host_chunks(images, per_image, host_chunk_bytes(), host_ramp());
     const int nchunks = static_cast<int>(sizes.size());
     while (static_cast<int>(hs.ev_in.size()) < nchunks) {
         cudaEvent_t a = nullptr, b = nullptr;
-        SPCV_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
-        SPCV_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        SPCV_HOST_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
         hs.ev_in.push_back(a);
+        SPCV_HOST_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
         hs.ev_done.push_back(b);
     }
     const size_t in_img = S * act_c, out_img = S * out_c;
     if (n_bias)
-        SPCV_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice, hs.h2d));
+        SPCV_HOST_CUDA(cudaMemcpyAsync(d_bias, bias, n_bias * sizeof(float), cudaMemcpyHostToDevice, hs.h2d));
     for (int c = 0, i0 = 0; c < nchunks; i0 += sizes[c], ++c) {
-        const int ni = sizes[c];
-        SPCV_CUDA(cudaMemcpyAsync(d_act + i0 * in_img, act + i0 * in_img, ni * in_img * sizeof(float),
-                                  cudaMemcpyHostToDevice, hs.h2d));
-        SPCV_CUDA(cudaEventRecord(hs.ev_in[c], hs.h2d));
-        SPCV_CUDA(cudaStreamWaitEvent(hs.k, hs.ev_in[c], 0));
-        rc = launch(w, d_act + i0 * in_img, ni, act_h, act_w, d_bias, act_kind, lo, hi,
-                    d_out + i0 * out_img, mode, hs.k);
-        if (rc) {
-            cudaStreamSynchronize(hs.h2d);
-            cudaStreamSynchronize(hs.k);
-            cudaSetDevice(prev);
-            return rc;
-        }
-        SPCV_CUDA(cudaEventRecord(hs.ev_done[c], hs.k));
-        SPCV_CUDA(cudaStreamWaitEvent(hs.d2h, hs.ev_done[c], 0));
-        SPCV_CUDA(cudaMemcpyAsync(out + i0 * out_img, d_out + i0 * out_img, ni * out_img * sizeof(float),
-                                  cudaMemcpyDeviceToHost, hs.d2h));
+        const size_t ni = static_cast<size_t>(sizes[c]), o = static_cast<size_t>(i0);
+        SPCV_HOST_CUDA(cudaMemcpyAsync(d_act + o * in_img, act + o * in_img, ni * in_img * sizeof(float),
+                                       cudaMemcpyHostToDevice, hs.h2d));
+        SPCV_HOST_CUDA(cudaEventRecord(hs.ev_in[c], hs.h2d));
+        SPCV_HOST_CUDA(cudaStreamWaitEvent(hs.k, hs.ev_in[c], 0));
+        rc = launch(w, d_act + o * in_img, sizes[c], act_h, act_w, d_bias, act_kind, lo, hi,
+                    d_out + o * out_img, mode, hs.k);
+        if (rc) return done(rc);
+        SPCV_HOST_CUDA(cudaEventRecord(hs.ev_done[c], hs.k));
+        SPCV_HOST_CUDA(cudaStreamWaitEvent(hs.d2h, hs.ev_done[c], 0));
+        SPCV_HOST_CUDA(cudaMemcpyAsync(out + o * out_img, d_out + o * out_img, ni * out_img * sizeof(float),
+                                       cudaMemcpyDeviceToHost, hs.d2h));
     }
-    SPCV_CUDA(cudaStreamSynchronize(hs.d2h));
-    SPCV_CUDA(cudaStreamSynchronize(hs.k));
-    cudaSetDevice(prev);
+    SPCV_HOST_CUDA(cudaStreamSynchronize(hs.d2h));
+    SPCV_HOST_CUDA(cudaStreamSynchronize(hs.k));
+#undef SPCV_HOST_CUDA
+    return done(SPCV_OK);
+}
+
+// ------------------------------------------------- the reference call shape
+// spmm_into(const BcsrMatrix&, ...) with host tensors, as one call. The
+// reference takes the matrix by const& on every call (kernels.cpp:304); here
+// it is packed once per distinct content and device and kept in a small LRU
+// cache, so a caller that loops spmm_into over layers and images (run_network,
+// bench_layers) never repacks, reschedules or recompiles. A hit is verified
+// byte for byte against the cached host copy (the hash only finds the entry).
+namespace {
+
+struct CachedWeights {
+    uint64_t hash = 0;
+    int device = 0, rows = 0, cols = 0, block_h = 0;
+    std::vector<uint32_t> row_ptr, col_idx;
+    std::vector<float> values;
+    std::shared_ptr<spcv_cu_weights> w;
+    size_t bytes() const { return (row_ptr.size() + col_idx.size() + values.size()) * 4; }
+};
+
+struct WeightCache {
+    std::mutex mu;
+    std::list<CachedWeights> lru;  // most recently used first
+    size_t bytes = 0;
+    uint64_t hits = 0, misses = 0;
+};
+WeightCache& weight_cache() {
+    static WeightCache* c = new WeightCache;  // never destroyed: no CUDA calls at exit
+    return *c;
+}
+
+size_t weight_cache_limit() {
+    static const size_t b = [] {
+        const char* e = std::getenv("SPCV_WEIGHT_CACHE_MB");
+        const long v = e ? std::atol(e) : 256;
+        return static_cast<size_t>(std::max(0L, v)) << 20;
+    }();
+    return b;
+}
+
+uint64_t hash_words(uint64_t h, const void* data, size_t bytes) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        uint64_t v;
+        std::memcpy(&v, p + i, 8);
+        h = (h ^ v) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 32;
+    }
+    for (; i < bytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+    return h ^ bytes;
+}
+
+}  // namespace
+
+extern "C" int spcv_cu_spmm_bcsr_into_host(int rows, int cols, int block_h, const uint32_t* row_ptr,
+                                           size_t row_ptr_len, const uint32_t* col_idx, size_t nblocks,
+                                           const float* values, size_t nvalues, const float* act,
+                                           int act_layout, int images, int act_c, int act_h, int act_w,
+                                           const float* bias, size_t bias_len, int act_kind, float lo,
+                                           float hi, float* out, int out_layout, int out_c, int out_h,
+                                           int out_w, int cfg_m, int cfg_n, int mode) {
+    g_last_error.clear();
+    {
+        // argument checks first, in the reference order, before the matrix is read
+        spcv_cu_weights shape;
+        shape.rows = rows;
+        shape.cols = cols;
+        shape.block_h = block_h;
+        const int rc = check_args(&shape, act_layout, images, act_c, act_h, act_w, bias_len, act_kind, lo, hi,
+                                  out_layout, out_c, out_h, out_w, cfg_m, cfg_n, mode);
+        if (rc) return rc;
+    }
+    int dev = 0;
+    SPCV_CUDA(cudaGetDevice(&dev));
+    const bool shapes_ok = row_ptr && row_ptr_len >= 1 && (nblocks == 0 || (col_idx && values));
+    uint64_t h = hash_words(0x243F6A8885A308D3ull ^ static_cast<uint64_t>(dev), &rows, sizeof rows);
+    h = hash_words(h, &cols, sizeof cols);
+    h = hash_words(h, &block_h, sizeof block_h);
+    if (shapes_ok) {
+        h = hash_words(h, row_ptr, row_ptr_len * 4);
+        h = hash_words(h, col_idx, nblocks * 4);
+        h = hash_words(h, values, nvalues * 4);
+    }
+    std::shared_ptr<spcv_cu_weights> w;
+    WeightCache& c = weight_cache();
+    if (shapes_ok) {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
+            if (it->hash == h && it->device == dev && it->rows == rows && it->cols == cols &&
+                it->block_h == block_h && it->row_ptr.size() == row_ptr_len && it->col_idx.size() == nblocks &&
+                it->values.size() == nvalues && std::memcmp(it->row_ptr.data(), row_ptr, row_ptr_len * 4) == 0 &&
+                (nblocks == 0 || std::memcmp(it->col_idx.data(), col_idx, nblocks * 4) == 0) &&
+                (nvalues == 0 || std::memcmp(it->values.data(), values, nvalues * 4) == 0)) {
+                c.lru.splice(c.lru.begin(), c.lru, it);
+                w = it->w;
+                ++c.hits;
+                break;
+            }
+    }
+    if (!w) {
+        spcv_cu_weights* raw = nullptr;
+        const int rc = spcv_cu_pack(rows, cols, block_h, row_ptr, row_ptr_len, col_idx, nblocks, values,
+                                    nvalues, &raw);
+        if (rc) return rc;  // FormatError: a malformed matrix (never cached)
+        w = std::shared_ptr<spcv_cu_weights>(raw, [](spcv_cu_weights* p) { spcv_cu_free(p); });
+        CachedWeights e;
+        e.hash = h;
+        e.device = dev;
+        e.rows = rows;
+        e.cols = cols;
+        e.block_h = block_h;
+        e.row_ptr.assign(row_ptr, row_ptr + row_ptr_len);
+        e.col_idx.assign(col_idx, col_idx + nblocks);
+        e.values.assign(values, values + nvalues);
+        e.w = w;
+        std::lock_guard<std::mutex> lk(c.mu);
+        ++c.misses;
+        const size_t limit = weight_cache_limit();
+        if (e.bytes() <= limit) {
+            c.bytes += e.bytes();
+            c.lru.push_front(std::move(e));
+            while (c.bytes > limit && !c.lru.empty()) {  // evict the least recently used
+                c.bytes -= c.lru.back().bytes();
+                c.lru.pop_back();  // in-flight callers hold their own reference
+            }
+        }
+    }
+    return spcv_cu_spmm_into_host(w.get(), act, act_layout, images, act_c, act_h, act_w, bias, bias_len,
+                                  act_kind, lo, hi, out, out_layout, out_c, out_h, out_w, cfg_m, cfg_n, mode);
+}
+
+extern "C" void spcv_cu_weight_cache_clear(void) {
+    WeightCache& c = weight_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.lru.clear();
+    c.bytes = 0;
+}
+
+extern "C" int spcv_cu_cache_stats(size_t* entries, uint64_t* hits, uint64_t* misses, uint64_t* jit_compiles,
+                                   uint64_t* jit_disk_hits) {
+    WeightCache& c = weight_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (entries) *entries = c.lru.size();
+    if (hits) *hits = c.hits;
+    if (misses) *misses = c.misses;
+    if (jit_compiles) *jit_compiles = g_jit_compiles.load();
+    if (jit_disk_hits) *jit_disk_hits = g_jit_cache_hits.load();
     return SPCV_OK;
 }
 

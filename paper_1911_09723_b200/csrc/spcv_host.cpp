@@ -246,13 +246,15 @@ void spmm_into(const BcsrMatrix& w, const Tensor& act, std::span<const float> bi
     const int m = cfg.m != 0 ? cfg.m : default_strip_width(cfg.tier);
     if (m != 4 && m != 8 && m != 16) throw std::invalid_argument("spmm: strip width must be 4, 8 or 16");
 
-    const DeviceBcsr dw(w);
-    check(spcv_cu_spmm_into_host(dw.handle(), act.data.data(), layout_code(act.layout), 1,
-                                 act.channels, act.height, act.width,
-                                 bias.empty() ? nullptr : bias.data(), bias.size(),
-                                 act_kind(fused), fused.lo, fused.hi, out.data.data(),
-                                 layout_code(out.layout), out.channels, out.height, out.width,
-                                 cfg.m, cfg.n, cfg.strict ? SPCV_MODE_STRICT : SPCV_MODE_FAST));
+    // packed once per distinct matrix content (the C-ABI's weight cache): a
+    // caller looping spmm_into over layers and images never repacks
+    check(spcv_cu_spmm_bcsr_into_host(w.rows, w.cols, w.block_h, w.row_ptr.data(), w.row_ptr.size(),
+                                      w.col_idx.data(), w.col_idx.size(), w.values.data(), w.values.size(),
+                                      act.data.data(), layout_code(act.layout), 1, act.channels,
+                                      act.height, act.width, bias.empty() ? nullptr : bias.data(),
+                                      bias.size(), act_kind(fused), fused.lo, fused.hi, out.data.data(),
+                                      layout_code(out.layout), out.channels, out.height, out.width,
+                                      cfg.m, cfg.n, cfg.strict ? SPCV_MODE_STRICT : SPCV_MODE_FAST));
 }
 
 Tensor spmm(const BcsrMatrix& w, const Tensor& act, std::span<const float> bias,

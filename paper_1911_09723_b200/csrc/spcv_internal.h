@@ -15,6 +15,27 @@
 #include "../../include/spcv_cu.h"
 #include "spmm_kernel.cuh"
 
+// Tuning knobs (SPCV_* environment variables), read once when a
+// matrix is packed and kept in the weights object, so no launch reads the
+// environment. 0 / -1 = not set (the library's own choice).
+struct Knobs {
+    int steps = 0;         // SPCV_STEPS: 2 or 4 steps per chunk
+    int nf = 0;            // SPCV_NF: 2 or 4 float4 quads per lane
+    int tile_t = 0;        // SPCV_TILE_T: 32 / 64 / 128 columns per tile
+    int nwarps = 0;        // SPCV_NWARPS: 4 / 8 / 16 warps per CTA
+    int split = 0;         // SPCV_SPLIT: CTAs per tile (power of two)
+    int tail = -1;         // SPCV_TAIL: 0 = no tail split, n = n row slices
+    bool autotune = true;  // SPCV_AUTOTUNE=0: tail split from the heuristic only
+    bool jit = true;       // SPCV_JIT=0: the tile kernel everywhere
+    bool fuse_dw = false;  // SPCV_FUSE_DW=1: depthwise fused into the next 1x1 (executor, opt-in)
+    long long kmajor_min_cols = -1;  // SPCV_JIT_KMAJOR_MIN_COLS
+    int jit_warps = 0, jit_stages = 0;                 // SPCV_JIT_WARPS / SPCV_JIT_STAGES
+    int jit_seg_instr = 0, jit_max_segs = 0;           // SPCV_JIT_SEG_INSTR / SPCV_JIT_MAX_SEGS
+    int jit_direct_maxk = 0, jit_interleave = 1;       // SPCV_JIT_DIRECT_MAXK / SPCV_JIT_INTERLEAVE
+    static Knobs from_env();
+    long long geometry_key() const { return (static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1; }
+};
+
 // A weight-specialised kernel compiled at run time (jit.cu), one per call
 // shape: arithmetic mode, activation kind, bias/residual presence, stored
 // rows, 16 B-vectorisable activations, SM count of the device.
@@ -47,8 +68,10 @@ struct JitDwArgs {
 };
 struct JitVariant {
     JitKey key;
+    bool eligible = false;      // the planner found a variant for (matrix, key)
+    bool built = false;         // compile + load attempted (fn null: it failed)
     cudaLibrary_t lib = nullptr;
-    cudaKernel_t fn = nullptr;  // null: not built (ineligible, or compile/load failed)
+    cudaKernel_t fn = nullptr;
     bool direct = false;        // one thread per column (small K) vs k-major segments
     int cpl = 2;                // k-major: columns per lane (2 = f32x2, 1 = scalar)
     int segments = 0;
@@ -74,11 +97,13 @@ struct spcv_cu_weights {
     uint32_t* d_bin_beg = nullptr;
     uint4* d_stream_fast = nullptr;     // null: fast mode shares the strict stream
     uint32_t* d_bin_beg_fast = nullptr;
-    // small-K path (jit.cu): host copy of the matrix and the compiled variants
+    Knobs knobs;  // tuning knobs at pack time
+    // small-K path (jit.cu): host copy of the matrix and the planned / compiled
+    // variants (a cache inside a const weights object: mutable, guarded by jit.cu's mutex)
     bool jit_eligible = false;
     std::vector<uint32_t> h_row_ptr, h_col_idx;
     std::vector<float> h_values;
-    std::deque<JitVariant> jit;  // deque: variants never move (launching threads hold pointers)
+    mutable std::deque<JitVariant> jit;  // deque: variants never move (launching threads hold pointers)
     // Channel passes (K too wide for one shared-memory tile): the matrix split
     // by input-channel range, each part packed on its own; a call runs them in
     // channel order, each continuing the previous part's sums (spcv_cu.cu)
@@ -92,6 +117,7 @@ struct spcv_cu_weights {
 namespace spcv_detail {
 
 extern std::atomic<uint64_t> g_launches;
+extern std::atomic<uint64_t> g_jit_compiles, g_jit_cache_hits;  // NVRTC compiles / on-disk cubin hits
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 
@@ -122,8 +148,15 @@ constexpr int kJitDirectMaxK = 64;  // direct variant: activations of a column i
 constexpr int kJitWarps = 8;
 constexpr int kJitStages = 3;
 inline int jit_smem_bytes(int warps, int stages, int cpl = 2) { return warps * stages * 32 * 32 * cpl * 4; }
-void jit_geometry(JitKey& key);  // warps/stages (SPCV_JIT_WARPS / SPCV_JIT_STAGES override)
-const JitVariant* jit_prepare(spcv_cu_weights* w, const JitKey& key);  // null: unavailable
+void jit_geometry(JitKey& key, const Knobs& kn);  // warps/stages (knobs override)
+// Plan (cheap: no compile) the variant serving (matrix, key); null when none does.
+const JitVariant* jit_plan(const spcv_cu_weights* w, const JitKey& key);
+// Compile + load a planned variant on first use (NVRTC, or the on-disk cubin
+// cache); null when that fails (recorded, never retried).
+const JitVariant* jit_build(const spcv_cu_weights* w, const JitVariant* v);
+inline const JitVariant* jit_prepare(const spcv_cu_weights* w, const JitKey& key) {
+    return jit_build(w, jit_plan(w, key));
+}
 int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st,
                const JitDwArgs* dw = nullptr);
 // Depthwise 3x3 (host copies of its weights/bias) fused into the next sparse

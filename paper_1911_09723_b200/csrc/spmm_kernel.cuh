@@ -20,14 +20,8 @@
 //    packer (row bucketing + LPT, see spcv_cu.cu). Every chunk is 4 steps of
 //    (smem byte offset, block values) for each of the G rows; a register ring
 //    keeps chunks in flight to cover L2 latency.
-//  * Two kernels share the row-group executor (struct Exec):
-//      spmm_bcsr_kernel     — one tile per CTA, all warps stage with cp.async
-//                             (any H*W, any alignment);
-//      spmm_bcsr_pipelined  — persistent CTA per SM, one producer warp feeding
-//                             an NS-stage shared-memory ring with bulk async
-//                             copies (cp.async.bulk + mbarrier complete_tx)
-//                             while the consumer warps compute the previous
-//                             tiles (H*W % 4 == 0, 16 B-aligned tensors).
+//  * spmm_bcsr_kernel: one tile per CTA, all warps stage it with cp.async
+//    (any H*W, any alignment), then run the row-group executor (struct Exec).
 //  * STRICT uses separately rounded multiply and add (__fmul_rn/__fadd_rn),
 //    reproducing the reference bit-for-bit; !STRICT uses FFMA.
 #pragma once
@@ -543,203 +537,6 @@ spmm_bcsr_kernel(const KernelArgs a) {
     for (int d = 0; d < kRing; ++d)
         if (pos + d < end) ex.consume(ring[d], a);
     ex.finish(a);
-}
-
-// ---------------------------------------------------------------- kernel 2
-// Persistent, warp-specialised pipeline (H*W % 4 == 0, 16 B-aligned tensors):
-// warps 0..W-1 consume tiles, warp W produces them. The producer fills an
-// NS-stage ring of [K+1][T] tiles with cp.async.bulk row segments completing
-// on the stage's "full" mbarrier (expect_tx = the stage's bytes); consumers
-// wait on "full", compute, and arrive on the stage's "empty" mbarrier. The
-// weight stream is read as one continuous ring across tiles (the same chunk
-// sequence repeats per tile), so L2 latency stays hidden at tile boundaries.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-#ifndef SPCV_PIPE_CONSUMERS
-#define SPCV_PIPE_CONSUMERS 8
-#endif
-constexpr int kPipeConsumers = SPCV_PIPE_CONSUMERS;  // consumer warps per CTA
-constexpr int kPipeThreads = (kPipeConsumers + 1) * 32;
-constexpr int kPipeMaxStages = 4;
-
-template <int BH, int LPR, int NF, bool STRICT>
-__global__ void __launch_bounds__(kPipeThreads, 1)
-spmm_bcsr_pipelined(const KernelArgs a, int nstages, long long ntiles) {
-    constexpr int STEPS = 4;
-    using E = Exec<BH, LPR, NF, STEPS, STRICT, true>;
-    constexpr int G = E::G;
-    constexpr int T = E::T;
-    constexpr int kRing = BH == 1 ? 3 : 2;
-
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const size_t act_bytes = static_cast<size_t>(a.K + 1) * T * 4;
-    const size_t stage_bytes = act_bytes + static_cast<size_t>(T) * 8;   // tile + column offsets
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);              // full[NS], empty[NS]
-    float* s_bias = reinterpret_cast<float*>(smem_raw + 2 * kPipeMaxStages * 8);
-    unsigned char* stages = smem_raw + 2 * kPipeMaxStages * 8 +
-                            ((static_cast<size_t>(a.M) * 4 + 127) & ~static_cast<size_t>(127));
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-
-    if (tid == 0) {
-        for (int s = 0; s < nstages; ++s) {
-            mbar_init(&bars[s], 1);                       // full: producer's arrive + tx bytes
-            mbar_init(&bars[kPipeMaxStages + s], kPipeConsumers);  // empty: one per consumer warp
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (a.bias != nullptr)
-        for (int i = tid; i < a.M; i += blockDim.x) s_bias[i] = i < a.M_out ? __ldg(a.bias + i) : 0.0f;
-    for (int s = 0; s < nstages; ++s) {  // zero rows (never overwritten by copies)
-        float* zr = reinterpret_cast<float*>(stages + s * stage_bytes) + static_cast<size_t>(a.K) * T;
-        for (int i = tid; i < T; i += blockDim.x) zr[i] = 0.f;
-    }
-    __syncthreads();
-
-    const long long KS = static_cast<long long>(a.K) * a.S;
-
-    if (warp == kPipeConsumers) {
-        // ------------------------------------------------------ producer
-        long long i = 0;
-        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-            const int st = static_cast<int>(i % nstages);
-            if (i >= nstages) mbar_wait(&bars[kPipeMaxStages + st], static_cast<uint32_t>((i / nstages - 1) & 1));
-            unsigned char* sb = stages + st * stage_bytes;
-            float* s_act = reinterpret_cast<float*>(sb);
-            long long* s_col = reinterpret_cast<long long*>(sb + act_bytes);
-            const long long n0 = tile * T;
-            const int vc = static_cast<int>(min(static_cast<long long>(T), a.N - n0));  // valid columns
-            if (lane == 0) mbar_expect_tx(&bars[st], static_cast<uint32_t>(a.K) * vc * 4u);
-            __syncwarp();
-            // row segments: columns [c0, c0+len) of one image are contiguous per row k
-            for (int c0 = 0; c0 < vc;) {
-                const long long n = n0 + c0;
-                const long long b = n / a.S;
-                const int s0 = static_cast<int>(n - b * a.S);
-                const int len = min(vc - c0, a.S - s0);
-                const float* src = a.act + b * KS + s0;
-                for (int k = lane; k < a.K; k += 32)
-                    bulk_g2s(s_act + static_cast<size_t>(k) * T + c0, src + static_cast<long long>(k) * a.S,
-                             static_cast<uint32_t>(len) * 4u, &bars[st]);
-                c0 += len;
-            }
-            if (vc < T)  // past the last column: zeros (generic-proxy stores)
-                for (int e = lane; e < a.K * (T - vc); e += 32)
-                    s_act[static_cast<size_t>(e / (T - vc)) * T + vc + e % (T - vc)] = 0.f;
-            for (int c = lane; c < T; c += 32) s_col[c] = col_offset(n0 + c, a);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars[st]);
-        }
-        return;
-    }
-
-    // ---------------------------------------------------------- consumers
-    const int gi = lane / LPR;
-    const int per = kBins / (kPipeConsumers * gridDim.y);
-    const int bin0 = (blockIdx.y * kPipeConsumers + warp) * per;
-    const uint32_t beg = __ldg(a.bin_beg + bin0);
-    const uint32_t end = __ldg(a.bin_beg + bin0 + per);
-    const uint32_t L = end - beg;  // chunks per tile for this warp
-    const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-
-    E ex;
-    ex.init(gi, lane % LPR, s_bias, a.bias != nullptr);
-
-    if (L == 0) {  // no rows for this warp: keep the stage handshake going
-        for (long long i = 0; i < my_tiles; ++i) {
-            const int st = static_cast<int>(i % nstages);
-            mbar_wait(&bars[st], static_cast<uint32_t>((i / nstages) & 1));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars[kPipeMaxStages + st]);
-        }
-        return;
-    }
-
-    // continuous chunk sequence: tile after tile, the same L chunks each time
-    const long long total = static_cast<long long>(L) * my_tiles;
-    uint32_t lpos = beg;      // next chunk to load (wraps at end)
-    long long loaded = 0;
-    auto next_load = [&]() {
-        if (loaded >= total) return zero_chunk<BH, STEPS>();
-        const Chunk<BH, STEPS> ch = load_chunk<BH, G, STEPS>(a.stream, lpos, gi);
-        lpos = lpos + 1 == end ? beg : lpos + 1;
-        ++loaded;
-        return ch;
-    };
-    Chunk<BH, STEPS> ring[kRing];
-#pragma unroll
-    for (int d = 0; d < kRing; ++d) ring[d] = next_load();
-
-    long long tile_i = -1;    // index of the tile being consumed
-    uint32_t cpos = 0;        // position within the tile's L chunks
-    auto step = [&](const Chunk<BH, STEPS>& cur) {
-        if (cpos == 0) {      // tile boundary: release the old stage, acquire the next
-            if (tile_i >= 0) {
-                ex.finish(a);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars[kPipeMaxStages + static_cast<int>(tile_i % nstages)]);
-            }
-            ++tile_i;
-            const int st = static_cast<int>(tile_i % nstages);
-            mbar_wait(&bars[st], static_cast<uint32_t>((tile_i / nstages) & 1));
-            ex.s_bytes = reinterpret_cast<const char*>(stages + st * stage_bytes);
-            ex.s_col = reinterpret_cast<const long long*>(stages + st * stage_bytes + act_bytes);
-            ex.set_tile((blockIdx.x + tile_i * static_cast<long long>(gridDim.x)) * T, a);
-        }
-        ex.consume(cur, a);
-        cpos = cpos + 1 == L ? 0 : cpos + 1;
-    };
-    long long done = 0;
-    while (done + kRing <= total) {
-#pragma unroll
-        for (int d = 0; d < kRing; ++d) {
-            const Chunk<BH, STEPS> cur = ring[d];
-            ring[d] = next_load();
-            ++done;
-            step(cur);
-        }
-    }
-#pragma unroll
-    for (int d = 0; d < kRing; ++d)
-        if (done + d < total) step(ring[d]);
-    ex.finish(a);
-    __syncwarp();
-    if (lane == 0 && tile_i >= 0) mbar_arrive(&bars[kPipeMaxStages + static_cast<int>(tile_i % nstages)]);
 }
 
 }  // namespace spcvk

@@ -156,14 +156,21 @@ def spmm_into(w, act: Tensor, bias, fused: Activation, out: Tensor,
     m = cfg.m if cfg.m != 0 else default_strip_width(cfg.tier)
     if m not in (4, 8, 16):
         raise ValueError("spmm: strip width must be 4, 8 or 16")
-    dw = w if isinstance(w, DeviceBcsr) else DeviceBcsr(w)
     a = np.ascontiguousarray(act.data, np.float32)
     if out.data.dtype != np.float32 or not out.data.flags.c_contiguous:
         out.data = np.ascontiguousarray(out.data, np.float32)
-    _raise(lib.spcv_cu_spmm_into_host(
-        dw.handle, _ptr(a), int(act.layout), 1, act.channels, act.height, act.width,
-        _ptr(b) or None, b.size, fused.kind, fused.lo, fused.hi, _ptr(out.data), int(out.layout),
-        out.channels, out.height, out.width, cfg.m, cfg.n, _mode(cfg)))
+    tail = (_ptr(a), int(act.layout), 1, act.channels, act.height, act.width,
+            _ptr(b) or None, b.size, fused.kind, fused.lo, fused.hi, _ptr(out.data), int(out.layout),
+            out.channels, out.height, out.width, cfg.m, cfg.n, _mode(cfg))
+    if isinstance(w, DeviceBcsr):
+        _raise(lib.spcv_cu_spmm_into_host(w.handle, *tail))
+        return
+    # a host BcsrMatrix: packed once per distinct content (spcv_cu_spmm_bcsr_into_host's cache)
+    rp = np.ascontiguousarray(w.row_ptr, dtype=np.uint32)
+    ci = np.ascontiguousarray(w.col_idx, dtype=np.uint32)
+    va = np.ascontiguousarray(w.values, dtype=np.float32)
+    _raise(lib.spcv_cu_spmm_bcsr_into_host(int(w.rows), int(w.cols), int(w.block_h), _ptr(rp), rp.size,
+                                           _ptr(ci), ci.size, _ptr(va), va.size, *tail))
 
 
 def spmm(w, act: Tensor, bias, fused: Activation | None = None,
@@ -182,8 +189,17 @@ def spmm_host_batched(w: DeviceBcsr, act: np.ndarray, bias, fused: Activation, o
     """Batched host path: act [B][K][H][W] -> out [B][M][H][W] (numpy, ideally pinned)
     through spcv_cu_spmm_into_host (H2D, kernel, D2H inside the call)."""
     cfg = cfg or MicrokernelConfig(n=w.block_h)
+    if not isinstance(act, np.ndarray) or act.ndim != 4:
+        raise ShapeError("spmm_host_batched: act must be a [B][K][H][W] numpy array")
+    if act.dtype != np.float32 or not act.flags.c_contiguous:
+        act = np.ascontiguousarray(act, dtype=np.float32)  # a copy (a pinned act should be float32 C-order)
     B, K, H, W = act.shape
-    b = None if bias is None else np.ascontiguousarray(bias, np.float32)
+    if (not isinstance(out, np.ndarray) or out.dtype != np.float32 or not out.flags.c_contiguous
+            or not out.flags.writeable):
+        raise ShapeError("spmm_host_batched: out must be a writeable C-contiguous float32 numpy array")
+    if out.shape != (B, w.rows, H, W):
+        raise ShapeError(f"spmm_host_batched: out shape {out.shape} != {(B, w.rows, H, W)}")
+    b = None if bias is None else np.ascontiguousarray(bias, np.float32).reshape(-1)
     _raise(lib.spcv_cu_spmm_into_host(
         w.handle, act.ctypes.data, _capi.LAYOUT_CHW, B, K, H, W,
         None if b is None else b.ctypes.data, 0 if b is None else b.size, fused.kind, fused.lo,
@@ -331,7 +347,16 @@ class DeviceModel:
         in forward()."""
         import torch
 
+        L = self.layers[i]
         B = act.shape[0]
+        for name, t, per in (("act", act, L["cin"] * L["in_h"] * L["in_w"]),
+                             ("out", out, L["cout"] * L["out_h"] * L["out_w"]),
+                             ("residual", residual, L["cout"] * L["out_h"] * L["out_w"])):
+            if t is None:
+                continue
+            if (t.device.type != "cuda" or t.device != act.device or t.dtype != torch.float32
+                    or not t.is_contiguous() or t.numel() != B * per):
+                raise ShapeError(f"run: {name} must be a contiguous float32 CUDA tensor of {B}x{per} elements")
         if stream is None:
             stream = torch.cuda.current_stream(act.device)
         sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
@@ -346,11 +371,17 @@ class DeviceModel:
         input/output tensors on a non-default stream replays a CUDA graph)."""
         import torch
 
+        if images_hwc.device.type != "cuda" or images_hwc.dtype != torch.float32 or images_hwc.dim() != 4:
+            raise DeviceError("forward: images must be a [B][H][W][C] float32 CUDA tensor")
         x = images_hwc.contiguous()
         B, H, W, C = x.shape
         classes = self.layers[-1]["cout"]
         if out is None:
             out = torch.empty((B, classes), dtype=torch.float32, device=x.device)
+        elif (out.device != x.device or out.dtype != torch.float32 or not out.is_contiguous()
+              or tuple(out.shape) != (B, classes)):
+            raise ShapeError(f"forward: out must be a contiguous float32 tensor of shape {(B, classes)} "
+                             f"on {x.device}")
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream

@@ -486,6 +486,76 @@ def test_wide_matrices_run_as_channel_passes_bit_exact(oracle, case):
                           np.asarray(m.values, np.float32).view(np.uint32))
 
 
+@pytest.mark.parametrize("images", [1, 4, 5, 9])
+def test_host_path_large_images_chunking(oracle, images):
+    """Host-buffer entry point with one image larger than half the 48 MiB chunk
+    budget (chunk = 1 image): the chunk schedule must cover exactly `images`
+    images (the ramp used to overrun the buffers at 4-5 images)."""
+    rng = np.random.default_rng(100 + images)
+    K = M = 64
+    H = W = 224  # (64+64)*224*224*4 B = 25.7 MB per image
+    dense = (rng.standard_normal((M, K)) * 0.1).astype(np.float32)
+    dense *= rng.random((M, K)) >= 0.9
+    m = sp.encode_bcsr(dense, 1)
+    act_ = rng.uniform(-1, 1, (images, K, H, W)).astype(np.float32)
+    bias = (rng.standard_normal(M) * 0.1).astype(np.float32)
+    want = oracle.spmm(m, act_, bias, RELU6, nthreads=8).reshape(images, M, H, W)
+    guard = 8
+    buf = np.full((images + guard, M, H, W), np.nan, np.float32)  # images past `images` must stay untouched
+    host_out = buf[:images]
+    sp.spmm_host_batched(sp.DeviceBcsr(m), act_, bias, RELU6, host_out, sp.MicrokernelConfig(n=1))
+    assert np.array_equal(bits(host_out), bits(want))
+    assert np.isnan(buf[images:]).all()
+
+
+def test_host_path_rejects_bad_outputs():
+    m = sp.encode_bcsr(np.eye(8, dtype=np.float32), 1)
+    w = sp.DeviceBcsr(m)
+    act_ = np.ones((2, 8, 3, 3), np.float32)
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_host_batched(w, act_, None, NONE, np.zeros((1, 8, 3, 3), np.float32))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_host_batched(w, act_, None, NONE, np.zeros((2, 8, 3, 3), np.float64))
+    with pytest.raises(sp.ShapeError):
+        sp.spmm_host_batched(w, act_, None, NONE, np.zeros((2, 8, 3, 3), np.float32)[:, :, :, ::-1])
+    out = np.zeros((2, 8, 3, 3), np.float32)
+    sp.spmm_host_batched(w, act_.astype(np.float64), None, NONE, out)  # act converted
+    assert np.array_equal(out, np.ones_like(out))
+
+
+def test_reference_call_shape_packs_and_compiles_once(oracle, tmp_path, monkeypatch):
+    """spmm_into(BcsrMatrix, host tensors) in a loop (the reference's callers,
+    run_network / bench_layers): the matrix is packed once per content, the
+    weight-specialised kernel compiled at most once, every result bit-exact;
+    a different matrix of the same shape is a different cache entry."""
+    d = make_layer_data(Layer("loop", 48, 96, 6, 6, sparsity=0.85), 3, 321)  # K <= 64: JIT direct
+    s0 = sp.cache_stats()
+    for i in range(3):
+        out = sp.spmm(d.weights, sp.Tensor(48, 6, 6, data=d.act[i]), d.bias, RELU6)
+        want = oracle.spmm(d.weights, d.act[i:i + 1], d.bias, RELU6).reshape(-1)
+        assert np.array_equal(bits(out.data), bits(want))
+    s1 = sp.cache_stats()
+    assert s1["misses"] - s0["misses"] == 1 and s1["hits"] - s0["hits"] == 2
+    assert s1["jit_compiles"] + s1["jit_disk_hits"] - s0["jit_compiles"] - s0["jit_disk_hits"] <= 1
+    other = sp.BcsrMatrix(d.weights.rows, d.weights.cols, 1, d.weights.row_ptr, d.weights.col_idx,
+                          d.weights.values * np.float32(2.0))
+    sp.spmm(other, sp.Tensor(48, 6, 6, data=d.act[0]), d.bias, RELU6)
+    assert sp.cache_stats()["misses"] - s1["misses"] == 1
+
+
+def test_tile_kernel_matrix_never_compiles_jit(monkeypatch):
+    """A call the k-major JIT variant would not serve (too few columns) must not
+    compile it (the plan decides before NVRTC runs)."""
+    import torch
+
+    monkeypatch.delenv("SPCV_JIT_KMAJOR_MIN_COLS", raising=False)  # production threshold
+    d = make_layer_data(Layer("c1like", 128, 128, 28, 28, sparsity=0.8), 1, 5)
+    w = sp.DeviceBcsr(d.weights)
+    c0 = sp.cache_stats()["jit_compiles"]
+    run_device(d.weights, d.act, d.bias, RELU6, dw=w)
+    assert sp.cache_stats()["jit_compiles"] == c0
+
+
 def test_concurrent_streams_agree(oracle):
     import torch
 
@@ -506,7 +576,6 @@ def test_kernel_launches_are_counted():
 
 # ------------------------------------------- both kernels on the same inputs
 @pytest.mark.parametrize("layout", ["default", "steps2", "steps4", "nf2", "nf4_steps2"])
-@pytest.mark.parametrize("pipeline", ["0", "1"])
 @pytest.mark.parametrize("case", [
     ("pw3_b8", Layer("pw3", 128, 128, 56, 56, sparsity=0.9), 8),
     ("c3_bh4", Layer("c3", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.8, 4), 12),
@@ -514,12 +583,9 @@ def test_kernel_launches_are_counted():
     ("tail", Layer("tail", 64, 96, 6, 10, sparsity=0.7), 37),       # N % T != 0
     ("k1024", Layer("k", 1024, 256, 4, 4, sparsity=0.95), 300),     # 1-stage tile -> fallback
 ], ids=lambda c: c[0] if isinstance(c, tuple) else c)
-def test_pipelined_and_tile_kernels_bit_exact(oracle, monkeypatch, pipeline, case, layout):
-    """SPCV_PIPELINE forces the persistent bulk-copy pipeline (1) or the
-    one-tile-per-CTA kernel (0); SPCV_STEPS / SPCV_NF force the chunk length
-    and lane width the packer would otherwise pick. Every combination must
-    equal the oracle bit-for-bit."""
-    monkeypatch.setenv("SPCV_PIPELINE", pipeline)
+def test_tile_kernel_layouts_bit_exact(oracle, monkeypatch, case, layout):
+    """SPCV_STEPS / SPCV_NF force the chunk length and lane width the packer
+    would otherwise pick. Every combination must equal the oracle bit-for-bit."""
     monkeypatch.setenv("SPCV_JIT", "0")  # small K would otherwise take the JIT kernel
     env = {"steps2": {"SPCV_STEPS": "2"}, "steps4": {"SPCV_STEPS": "4"}, "nf2": {"SPCV_NF": "2"},
            "nf4_steps2": {"SPCV_NF": "4", "SPCV_STEPS": "2"}}.get(layout, {})
