@@ -65,6 +65,7 @@ Knobs Knobs::from_env() {
     k.jit_max_segs = static_cast<int>(get("SPCV_JIT_MAX_SEGS", 0));
     k.jit_direct_maxk = static_cast<int>(get("SPCV_JIT_DIRECT_MAXK", 0));
     k.jit_interleave = static_cast<int>(get("SPCV_JIT_INTERLEAVE", 1));
+    k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
     return k;
 }
 
@@ -190,7 +191,7 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
 // present in every part (empty where it has no block in the range). The
 // paper-format streams of the whole matrix are kept for spcv_cu_unpack.
 int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const uint32_t* col_idx, size_t nblocks,
-                const float* values, spcv_cu_weights** out) {
+                const float* values, spcv_cu_weights** out, int pass_channels) {
     const int brows = rows / block_h;
     auto* w = new (std::nothrow) spcv_cu_weights;
     if (!w) return fail(SPCV_ERR_CUDA, "spcv_cu_pack: out of host memory");
@@ -202,8 +203,8 @@ int pack_passes(int rows, int cols, int block_h, const uint32_t* row_ptr, const 
     w->knobs = Knobs::from_env();
     cudaGetDevice(&w->device);
     int rc = SPCV_OK;
-    for (int k0 = 0; k0 < cols && rc == SPCV_OK; k0 += kPassChannels) {
-        const uint32_t k1 = static_cast<uint32_t>(std::min(cols, k0 + kPassChannels));
+    for (int k0 = 0; k0 < cols && rc == SPCV_OK; k0 += pass_channels) {
+        const uint32_t k1 = static_cast<uint32_t>(std::min(cols, k0 + pass_channels));
         std::vector<uint32_t> rp(static_cast<size_t>(brows) + 1, 0), ci;
         std::vector<float> va;
         for (int r = 0; r < brows; ++r) {
@@ -302,7 +303,10 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     const Knobs kn = Knobs::from_env();
     const Layout lay = pass_part ? (block_h == 4 ? Layout{4, 2, 32} : Layout{2, 4, 32})
                                  : choose_layout(cols, rows, block_h, kn);
-    if (lay.LPR == 0 || cols >= 0xFFFF) return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out);
+    if (lay.LPR == 0 || cols >= 0xFFFF)
+        return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out, kPassChannels);
+    if (!pass_part && kn.pass_k > 0 && cols > kn.pass_k)  // tuning aid: narrower passes
+        return pack_passes(rows, cols, block_h, row_ptr, col_idx, nblocks, values, out, kn.pass_k);
     const int G = 32 / lay.LPR;
     const int T = lay.T;
     const int BH = block_h;
@@ -388,7 +392,7 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
         size_t total = 0;
         for (int g = 0; g < ngroups; ++g) total += 1 + gchunks[g];
         std::vector<unsigned char>& stream = out.stream;
-        stream.assign(total * CB + 16, 0);
+        stream.assign((total + 1) * CB, 0);  // + one padding chunk (ring stand-in past the end)
         out.bin_beg.assign(kBins + 1, 0);
         size_t cur = 0;
         auto idx_word = [&](size_t chunk, int slot, int wi) -> uint32_t* {

@@ -32,6 +32,7 @@ struct Knobs {
     int jit_warps = 0, jit_stages = 0;                 // SPCV_JIT_WARPS / SPCV_JIT_STAGES
     int jit_seg_instr = 0, jit_max_segs = 0;           // SPCV_JIT_SEG_INSTR / SPCV_JIT_MAX_SEGS
     int jit_direct_maxk = 0, jit_interleave = 1;       // SPCV_JIT_DIRECT_MAXK / SPCV_JIT_INTERLEAVE
+    int pass_k = 0;        // SPCV_PASS_K: run matrices wider than this as channel passes of this width
     static Knobs from_env();
     long long geometry_key() const { return (static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1; }
 };

@@ -28,6 +28,10 @@ KEYS = [
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe % (active)"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe % (active)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy % (active)"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe cycles active % (active)"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", "FMA-heavy pipe cycles % (active)"),
+    ("smsp__inst_executed.sum", "warp instructions executed"),
+    ("smsp__warps_eligible.avg.per_cycle_active", "eligible warps per cycle"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__block_size", "block size"),
