@@ -113,6 +113,7 @@ struct Layout {
 // leaves room for two CTAs per SM wins, else the widest that fits one CTA.
 // SPCV_NF=2|4 and SPCV_TILE_T=32|64|128 override (tuning aids).
 Layout choose_layout(int K, int M, int block_h, const Knobs& kn) {
+    if (block_h == 4 && kn.nf == 1 && smem_bytes(K, M, 32) <= kTwoCtaSmem) return {8, 1, 32};  // narrow
     int NF = (block_h == 4 || M <= 96) ? 2 : 4;
     if (block_h != 4 && (kn.nf == 2 || kn.nf == 4)) NF = kn.nf;  // tuning aid
     const int lprs_nf4[3] = {8, 4, 2};
@@ -327,6 +328,7 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     int steps_fast = short_rows ? 2 : 4;
     if (kn.steps == 2 || kn.steps == 4) steps_strict = steps_fast = kn.steps;
     if (pass_part) steps_strict = steps_fast = 4;
+    if (lay.NF == 1) steps_strict = steps_fast = 2;  // narrow layout: 4-step chunks would spill at 80 registers
 
     // paper-format streams
     std::vector<uint32_t> nnz(brows), delta(nblocks);

@@ -487,8 +487,17 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
 
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
+// Launch bounds per layout: the narrow block-height-4 layout (one quad per
+// lane) is built for three 8-warp CTAs per SM (<= 85 registers).
+template <int BH, int NF>
+struct Bounds {
+    static constexpr bool narrow = BH == 4 && NF == 1;
+    static constexpr int threads = narrow ? 256 : kThreads;
+    static constexpr int min_blocks = narrow ? 3 : kMinBlocks;
+};
+
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+__global__ void __launch_bounds__(Bounds<BH, NF>::threads, Bounds<BH, NF>::min_blocks)
 spmm_bcsr_kernel(const KernelArgs a) {
     using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
     constexpr int G = E::G;
