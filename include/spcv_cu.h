@@ -100,8 +100,21 @@ void spcv_cu_free(spcv_cu_weights* w);
  * spmm_into call shape). Both kernels are bit-exact in SPCV_MODE_STRICT.
  * SPCV_JIT=0 in the environment at pack time selects the tile kernel. No
  * reference counterpart (introspection). */
-enum { SPCV_KERNEL_TILE = 0, SPCV_KERNEL_JIT = 1 };
+enum { SPCV_KERNEL_TILE = 0, SPCV_KERNEL_JIT = 1, SPCV_KERNEL_SMALL = 2 };
 int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel);
+
+/* The kernel a spmm_into call of `images` act_h x act_w images (16 B-aligned
+ * tensors, bias, clamp) runs, which also depends on the column count:
+ *   SPCV_KERNEL_JIT     — as above (the k-major variant only with enough
+ *                         column groups for its persistent CTAs);
+ *   SPCV_KERNEL_SMALL   — fewer column tiles than SMs (batch 1, small planes):
+ *                         one warp per block row x 32 columns, activations
+ *                         gathered from global memory, no staging (small.cu);
+ *   SPCV_KERNEL_TILE    — everything else.
+ * All are bit-exact in SPCV_MODE_STRICT. SPCV_SMALL=0|2 at pack time
+ * disables / forces the few-column kernel. Compiles the JIT
+ * kernel if it is due. No reference counterpart (introspection). */
+int spcv_cu_weights_kernel_for(spcv_cu_weights* w, int mode, int images, int act_h, int act_w, int* kernel);
 
 /* spmm_into over a batch of `images` CHW images on device memory:
  *   act [images][act_c][act_h*act_w], out [images][out_c][out_h*out_w].
@@ -157,7 +170,7 @@ void spcv_cu_weight_cache_clear(void);
 int spcv_cu_cache_stats(size_t* entries, uint64_t* hits, uint64_t* misses, uint64_t* jit_compiles,
                         uint64_t* jit_disk_hits);
 
-/* The network executor's pointwise step/* The network executor's pointwise step (run_network, netdef.cpp:494-512) on
+/* The network executor's pointwise step (run_network, netdef.cpp:494-512) on
  * device tensors, fused: weights may carry padded rows (w.rows > out_c, up to
  * block_h-1 extra rows; they are computed with bias 0 and never stored, i.e.
  * the "run wide, keep the logical prefix" of netdef.cpp:496-505), and an

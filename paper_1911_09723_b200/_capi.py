@@ -23,6 +23,7 @@ SIGNATURES = {
     "spcv_cu_weights_info": (_i, [_p, _p, _p, _p, _p, _p, _p]),
     "spcv_cu_free": (None, [_p]),
     "spcv_cu_weights_kernel": (_i, [_p, _i, _p]),
+    "spcv_cu_weights_kernel_for": (_i, [_p, _i, _i, _i, _i, _p]),
     "spcv_cu_spmm_into": (_i, _SPMM_ARGS + [_p]),
     "spcv_cu_spmm_into_host": (_i, list(_SPMM_ARGS)),
     "spcv_cu_spmm_bcsr_into_host": (_i, [_i, _i, _i, _p, _z, _p, _z, _p, _z] + _SPMM_ARGS[1:]),
@@ -50,7 +51,10 @@ def _load() -> ctypes.CDLL:
             " (there is no CPU fallback)"
         )
     lib = ctypes.CDLL(LIB_PATH)
+    variant = bool(os.environ.get("SPCV_CU_LIB"))  # an A/B build may predate newer entry points
     for name, (res, args) in SIGNATURES.items():
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

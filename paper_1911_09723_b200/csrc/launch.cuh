@@ -97,9 +97,6 @@ int launch_s(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt,
 template <int BH>
 int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
               bool strict, bool vec, cudaStream_t st) {
-    if constexpr (BH == 4) {
-        if (w->NF == 1) return launch_s<BH, 8, 1>(a, w, nt, sms, strict, vec, st);  // narrow layout
-    }
     if (BH == 4 || w->NF == 2) {
         switch (w->LPR) {
             case 16: return launch_s<BH, 16, 2>(a, w, nt, sms, strict, vec, st);
@@ -132,8 +129,6 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     const Knobs& kn = w->knobs;
     for (int nw : {4, 8, 16}) {
         if (nw * 32 > spcvk::kThreads) continue;
-        cudaFuncAttributes fa{};
-        if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && nw * 32 > fa.maxThreadsPerBlock) continue;
         if (kn.nwarps && kn.nwarps != nw) continue;
         int ctas = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)

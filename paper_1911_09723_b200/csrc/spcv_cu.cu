@@ -66,6 +66,7 @@ Knobs Knobs::from_env() {
     k.jit_direct_maxk = static_cast<int>(get("SPCV_JIT_DIRECT_MAXK", 0));
     k.jit_interleave = static_cast<int>(get("SPCV_JIT_INTERLEAVE", 1));
     k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
+    k.small = static_cast<int>(get("SPCV_SMALL", 1));
     return k;
 }
 
@@ -113,7 +114,6 @@ struct Layout {
 // leaves room for two CTAs per SM wins, else the widest that fits one CTA.
 // SPCV_NF=2|4 and SPCV_TILE_T=32|64|128 override (tuning aids).
 Layout choose_layout(int K, int M, int block_h, const Knobs& kn) {
-    if (block_h == 4 && kn.nf == 1 && smem_bytes(K, M, 32) <= kTwoCtaSmem) return {8, 1, 32};  // narrow
     int NF = (block_h == 4 || M <= 96) ? 2 : 4;
     if (block_h != 4 && (kn.nf == 2 || kn.nf == 4)) NF = kn.nf;  // tuning aid
     const int lprs_nf4[3] = {8, 4, 2};
@@ -169,6 +169,8 @@ void free_weights(spcv_cu_weights* w) {
     cudaFree(w->d_bin_beg);
     cudaFree(w->d_stream_fast);
     cudaFree(w->d_bin_beg_fast);
+    cudaFree(w->d_row_ptr);
+    cudaFree(w->d_col_idx);
     for (spcv_cu_weights* p : w->parts) free_weights(p);
     jit_release(w);
     delete w;
@@ -328,7 +330,6 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     int steps_fast = short_rows ? 2 : 4;
     if (kn.steps == 2 || kn.steps == 4) steps_strict = steps_fast = kn.steps;
     if (pass_part) steps_strict = steps_fast = 4;
-    if (lay.NF == 1) steps_strict = steps_fast = 2;  // narrow layout: 4-step chunks would spill at 80 registers
 
     // paper-format streams
     std::vector<uint32_t> nnz(brows), delta(nblocks);
@@ -478,6 +479,8 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
         (rc = upload(&w->d_values, values, nvalues)) ||
         (rc = upload(&w->d_stream, reinterpret_cast<const uint4*>(bs.stream.data()), bs.stream.size() / 16)) ||
         (rc = upload(&w->d_bin_beg, bs.bin_beg.data(), bs.bin_beg.size())) ||
+        (rc = upload(&w->d_row_ptr, row_ptr, static_cast<size_t>(brows) + 1)) ||
+        (rc = upload(&w->d_col_idx, col_idx, nblocks)) ||
         (steps_fast != steps_strict &&
          ((rc = upload(&w->d_stream_fast, reinterpret_cast<const uint4*>(bf.stream.data()),
                        bf.stream.size() / 16)) ||
@@ -562,6 +565,37 @@ extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel)
 }
 
 // ------------------------------------------------------------------- launch
+namespace {
+int pick_kernel(const spcv_cu_weights* w, long long N, long long S, long long ntiles, int sms, bool vec, bool pass,
+                bool strict, bool clamp, bool has_bias, const float* residual, uintptr_t act, uintptr_t out,
+                int m_out, const JitVariant** jv);
+}  // namespace
+
+extern "C" int spcv_cu_weights_kernel_for(spcv_cu_weights* w, int mode, int images, int act_h, int act_w,
+                                          int* kernel) {
+    g_last_error.clear();
+    if (!w || !kernel) return fail(SPCV_ERR_INVALID, "spcv_cu_weights_kernel_for: null argument");
+    if (mode != SPCV_MODE_STRICT && mode != SPCV_MODE_FAST)
+        return fail(SPCV_ERR_INVALID, "spcv_cu_weights_kernel_for: unknown arithmetic mode");
+    if (images < 0 || act_h < 1 || act_w < 1) return fail(SPCV_ERR_SHAPE, "spcv_cu_weights_kernel_for: bad dims");
+    *kernel = SPCV_KERNEL_TILE;
+    if (!w->parts.empty()) return SPCV_OK;  // channel passes: the tile kernel
+    int prev = 0;
+    cudaGetDevice(&prev);
+    SPCV_CUDA(cudaSetDevice(w->device));
+    const long long S = static_cast<long long>(act_h) * act_w;
+    const long long N = S * images;
+    const long long ntiles = (N + w->T - 1) / w->T;
+    const int sms = props_for(w->device).sms;
+    const JitVariant* jv = nullptr;
+    // the spmm_into call shape on 16 B-aligned tensors: bias, clamp, all rows
+    int k = pick_kernel(w, N, S, ntiles, sms, S % 4 == 0, false, mode == SPCV_MODE_STRICT, true, true, nullptr,
+                        0, 0, w->rows, &jv);
+    if (k == SPCV_KERNEL_JIT && !jit_build(w, jv)) k = SPCV_KERNEL_TILE;  // launch()'s fallback after a failed compile
+    *kernel = k;
+    cudaSetDevice(prev);
+    return SPCV_OK;
+}
 
 namespace {
 
@@ -655,6 +689,45 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
     return best;
 }
 
+// Which kernel serves a call (spcv_cu_weights_kernel_for reports the same choice):
+//  * JIT — weight-specialised code (small K; the k-major variant only with
+//    enough column groups for its persistent CTAs: below that the other
+//    kernels' finer work units win — measured: c1, 784 columns, 24 vs 17 us;
+//    MBv2 384->64 @14x14 x128, 25088 columns in 2 segments, 53 vs 38 us);
+//    decided from the plan, so a variant that would not run is never compiled;
+//  * SMALL — fewer column tiles than SMs (batch 1, small planes): a warp per
+//    block row x 32 columns, gathers from global memory (small.cu);
+//  * TILE — everything else (any K, any layout, channel passes).
+int pick_kernel(const spcv_cu_weights* w, long long N, long long S, long long ntiles, int sms, bool vec, bool pass,
+                bool strict, bool clamp, bool has_bias, const float* residual, uintptr_t act, uintptr_t out,
+                int m_out, const JitVariant** jv) {
+    *jv = nullptr;
+    const Knobs& kn = w->knobs;
+    if (w->jit_eligible) {
+        JitKey key;
+        key.strict = strict;
+        key.clamp = clamp;
+        key.bias = has_bias;
+        key.res = residual != nullptr;
+        key.vec = S % 4 == 0 && act % 16 == 0 && out % 8 == 0 && reinterpret_cast<uintptr_t>(residual) % 8 == 0;
+        key.m_out = m_out;
+        key.sms = sms;
+        jit_geometry(key, kn);
+        if (const JitVariant* p = jit_plan(w, key)) {
+            const long long min_cols = kn.kmajor_min_cols >= 0
+                                           ? kn.kmajor_min_cols
+                                           : 32LL * p->cpl * sms * key.warps / std::max(1, p->segments);
+            if (p->direct || N >= min_cols) {
+                *jv = p;
+                return SPCV_KERNEL_JIT;
+            }
+        }
+    }
+    if (!pass && kn.small && w->d_row_ptr && w->brows <= 65535 * 4 && (kn.small > 1 || ntiles < sms))
+        return SPCV_KERNEL_SMALL;
+    return SPCV_KERNEL_TILE;
+}
+
 int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, int act_w,
            const float* bias, int act_kind, float lo, float hi, float* out, int mode,
            cudaStream_t st, int out_rows = -1, const float* residual = nullptr,
@@ -716,32 +789,18 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                      (reinterpret_cast<uintptr_t>(residual) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(acc_in) % 16 == 0);
     const bool strict = mode == SPCV_MODE_STRICT;
-    if (w->jit_eligible) {
-        // A failed compile (recorded, never retried) falls back to the tile kernel.
-        JitKey key;
-        key.strict = strict;
-        key.clamp = act_kind == SPCV_ACT_CLAMP;
-        key.bias = bias != nullptr;
-        key.res = residual != nullptr;
-        key.vec = S % 4 == 0 && reinterpret_cast<uintptr_t>(act) % 16 == 0 &&
-                  reinterpret_cast<uintptr_t>(out) % 8 == 0 &&
-                  reinterpret_cast<uintptr_t>(residual) % 8 == 0;
-        key.m_out = a.M_out;
-        key.sms = sms;
-        jit_geometry(key, w->knobs);
-        // The k-major variant is persistent (one CTA per SM, 32 or 64 columns
-        // per warp group, each segment on its share of the SMs): with fewer
-        // column groups than its warps the tile kernel's finer tiles win
-        // (measured: c1, 784 columns, 24 vs 17 us; MBv2 384->64 @14x14 x128,
-        // 25088 columns in 2 segments, 53 vs 38 us). Decided from the plan, so
-        // a variant that would not run is never compiled.
-        if (const JitVariant* p = jit_plan(w, key)) {
-            const long long min_cols = w->knobs.kmajor_min_cols >= 0
-                                           ? w->knobs.kmajor_min_cols
-                                           : 32LL * p->cpl * sms * key.warps / std::max(1, p->segments);
-            if (p->direct || N >= min_cols)
-                if (const JitVariant* v = jit_build(w, p)) return jit_launch(v, a, st);
-        }
+    const JitVariant* jv = nullptr;
+    const int kind = pick_kernel(w, N, S, ntiles, sms, vec, acc_in != nullptr || a.K_img != a.K, strict,
+                                 act_kind == SPCV_ACT_CLAMP, bias != nullptr, residual,
+                                 reinterpret_cast<uintptr_t>(act), reinterpret_cast<uintptr_t>(out), a.M_out, &jv);
+    if (kind == SPCV_KERNEL_JIT) {
+        // A failed compile (recorded, never retried) falls back to the other kernels.
+        if (const JitVariant* v = jit_build(w, jv)) return jit_launch(v, a, st);
+    }
+    if (kind == SPCV_KERNEL_SMALL) {
+        const int rc = launch_small(w, a, strict, st);
+        if (rc != SPCV_ERR_UNSUPPORTED) return rc;
+        g_last_error.clear();
     }
     auto run = [&](const spcvk::KernelArgs& args) {
         switch (w->block_h) {

@@ -33,6 +33,7 @@ struct Knobs {
     int jit_seg_instr = 0, jit_max_segs = 0;           // SPCV_JIT_SEG_INSTR / SPCV_JIT_MAX_SEGS
     int jit_direct_maxk = 0, jit_interleave = 1;       // SPCV_JIT_DIRECT_MAXK / SPCV_JIT_INTERLEAVE
     int pass_k = 0;        // SPCV_PASS_K: run matrices wider than this as channel passes of this width
+    int small = 1;         // SPCV_SMALL: 0 = never the few-column kernel, 2 = always (single pass)
     static Knobs from_env();
     long long geometry_key() const { return (static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1; }
 };
@@ -98,6 +99,14 @@ struct spcv_cu_weights {
     uint32_t* d_bin_beg = nullptr;
     uint4* d_stream_fast = nullptr;     // null: fast mode shares the strict stream
     uint32_t* d_bin_beg_fast = nullptr;
+    // row groups in LPT order, {first chunk, chunks} of d_stream / d_stream_fast
+    // (the persistent kernel takes them one at a time)
+    uint2* d_groups = nullptr;
+    // plain BCSR row_ptr / col_idx (d_values holds the blocks) for the few-column kernel (small.cu)
+    uint32_t* d_row_ptr = nullptr;
+    uint32_t* d_col_idx = nullptr;
+    uint2* d_groups_fast = nullptr;
+    int ngroups = 0;
     Knobs knobs;  // tuning knobs at pack time
     // small-K path (jit.cu): host copy of the matrix and the planned / compiled
     // variants (a cache inside a const weights object: mutable, guarded by jit.cu's mutex)
@@ -139,6 +148,9 @@ int launch_bh2(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
                bool strict, bool vec, cudaStream_t);
 int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntiles, int sms,
                bool strict, bool vec, cudaStream_t);
+// Few-column kernel (small.cu): one warp per block row x 32 columns, gathers
+// straight from global memory. SPCV_ERR_UNSUPPORTED when it cannot serve.
+int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& a, bool strict, cudaStream_t st);
 
 // Weight-specialised kernels (jit.cu): one persistent CTA of kJitWarps warps
 // per SM, a kJitStages-deep ring of [32 channels][64 columns] fp32 per warp.

@@ -191,20 +191,6 @@ __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a
 #define SPCV_HOIST 4
 #endif
 constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of their FMAs
-#ifndef SPCV_HOIST_BLOCK
-#define SPCV_HOIST_BLOCK SPCV_HOIST
-#endif
-// block heights >= 2: each step already carries 4*BH*NF FP instructions per lane
-constexpr int kHoistBlock = SPCV_HOIST_BLOCK;
-#ifndef SPCV_RING_AFTER
-#define SPCV_RING_AFTER 0
-#endif
-// Ring slots past the end of a warp's slice load chunk `end` (always present:
-// the next bin's first chunk or the stream's padding chunk) instead of
-// selecting a zero chunk; such slots are never consumed.
-#ifndef SPCV_NOZERO
-#define SPCV_NOZERO 0
-#endif
 
 // ACC: a channel pass — activations of K_img channels per image, and (after
 // the first pass) accumulators starting at acc_in. A separate instantiation,
@@ -350,10 +336,9 @@ struct Exec {
             return;
         }
         constexpr int kShift = T == 32 ? 7 : (T == 64 ? 8 : (T == 128 ? 9 : 10));  // log2(T*4)
-        constexpr int H = BH >= 2 ? kHoistBlock : kHoist;
 #pragma unroll
         for (int t = 0; t < STEPS; ++t) {
-            if (H < STEPS && t % H == 0 && t > 0) __syncwarp();
+            if (kHoist < STEPS && t % kHoist == 0 && t > 0) __syncwarp();
             const uint32_t word = cur.ix[t >> 1];
             const uint32_t off = ((t & 1) ? (word >> 16) : (word & 0xFFFFu)) << kShift;
             float4 x[NF];
@@ -418,10 +403,6 @@ __device__ __forceinline__ Chunk<BH, STEPS> load_chunk(const uint4* stream, uint
     return ch;
 }
 
-// Chunk c of a warp's slice [.., end), or a harmless stand-in past its end.
-template <int BH, int G, int STEPS>
-__device__ __forceinline__ Chunk<BH, STEPS> ring_chunk(const uint4* stream, uint32_t c, uint32_t end, int gi);
-
 template <int BH, int STEPS>
 __device__ __forceinline__ Chunk<BH, STEPS> zero_chunk() {
     Chunk<BH, STEPS> ch;
@@ -432,13 +413,10 @@ __device__ __forceinline__ Chunk<BH, STEPS> zero_chunk() {
     return ch;
 }
 
+// Chunk c of a warp's slice [.., end), or a zero chunk past its end (never consumed).
 template <int BH, int G, int STEPS>
 __device__ __forceinline__ Chunk<BH, STEPS> ring_chunk(const uint4* stream, uint32_t c, uint32_t end, int gi) {
-    if constexpr (SPCV_NOZERO) {
-        return load_chunk<BH, G, STEPS>(stream, c < end ? c : end, gi);
-    } else {
-        return c < end ? load_chunk<BH, G, STEPS>(stream, c, gi) : zero_chunk<BH, STEPS>();
-    }
+    return c < end ? load_chunk<BH, G, STEPS>(stream, c, gi) : zero_chunk<BH, STEPS>();
 }
 
 // Issue the cp.async copies of tile [n0, n0+T) into s_act [K][T] (16 B when
@@ -487,25 +465,13 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
 
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
-// Launch bounds per layout: the narrow block-height-4 layout (one quad per
-// lane) is built for three 8-warp CTAs per SM (<= 85 registers).
-template <int BH, int NF>
-struct Bounds {
-    static constexpr bool narrow = BH == 4 && NF == 1;
-    static constexpr int threads = narrow ? 256 : kThreads;
-    static constexpr int min_blocks = narrow ? 3 : kMinBlocks;
-};
-
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
-__global__ void __launch_bounds__(Bounds<BH, NF>::threads, Bounds<BH, NF>::min_blocks)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 spmm_bcsr_kernel(const KernelArgs a) {
     using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
     constexpr int G = E::G;
     constexpr int T = E::T;
-#ifndef SPCV_RING_BLOCK
-#define SPCV_RING_BLOCK 2
-#endif
-    constexpr int kRing = BH == 1 ? 3 : SPCV_RING_BLOCK;  // weight-stream chunks in flight per warp
+    constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
 
     extern __shared__ __align__(16) float smem[];
     float* s_act = smem;                                            // [K+1][T], row K = zeros
@@ -566,18 +532,10 @@ spmm_bcsr_kernel(const KernelArgs a) {
     while (pos + kRing <= end) {
 #pragma unroll
         for (int d = 0; d < kRing; ++d) {
-            if constexpr (SPCV_RING_AFTER) {
-                // consume in place, then refill the slot: no register copies of
-                // the chunk (the refill is hidden by the other kRing-1 chunks)
-                ex.consume(ring[d], a);
-                ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + kRing, end, gi);
-                ++pos;
-            } else {
-                const Chunk<BH, STEPS> cur = ring[d];
-                ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + kRing, end, gi);
-                ++pos;
-                ex.consume(cur, a);
-            }
+            const Chunk<BH, STEPS> cur = ring[d];
+            ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + kRing, end, gi);
+            ++pos;
+            ex.consume(cur, a);
         }
     }
 #pragma unroll

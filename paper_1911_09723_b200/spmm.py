@@ -107,6 +107,14 @@ class DeviceBcsr:
                                           ctypes.byref(k)))
         return "jit" if k.value == _capi.KERNEL_JIT else "tile"
 
+    def kernel_for(self, images: int, h: int, w: int, strict: bool = True) -> str:
+        """The kernel a call over `images` h x w images runs: "jit", "small"
+        or "tile" (spcv_cu_weights_kernel_for)."""
+        k = ctypes.c_int()
+        _raise(lib.spcv_cu_weights_kernel_for(self._h, _capi.MODE_STRICT if strict else _capi.MODE_FAST,
+                                              images, h, w, ctypes.byref(k)))
+        return _capi.KERNEL_NAMES[k.value]
+
     def unpack(self) -> BcsrMatrix:
         """Bit-exact device decode of the counts/deltas/values streams."""
         rp = np.zeros(self.rows // self.block_h + 1, dtype=np.uint32)

@@ -54,6 +54,17 @@ def run_device(m, act, bias, fused, strict=True, dw=None, stream=None):
     return o.cpu().numpy()
 
 
+def use_kernel(monkeypatch, kernel):
+    """Pack-time knobs that pick one kernel: "jit" (weight-specialised, where it
+    serves the matrix), "tile" (the shared-memory tile kernel) or "small" (the
+    few-column kernel)."""
+    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    monkeypatch.setenv("SPCV_SMALL", "2" if kernel == "small" else "0")
+
+
+KERNELS = ["jit", "tile", "small"]
+
+
 def load_cases():
     z = np.load(os.path.join(GOLD, "spmm_cases.npz"))
     cases = {}
@@ -586,7 +597,7 @@ def test_kernel_launches_are_counted():
 def test_tile_kernel_layouts_bit_exact(oracle, monkeypatch, case, layout):
     """SPCV_STEPS / SPCV_NF force the chunk length and lane width the packer
     would otherwise pick. Every combination must equal the oracle bit-for-bit."""
-    monkeypatch.setenv("SPCV_JIT", "0")  # small K would otherwise take the JIT kernel
+    use_kernel(monkeypatch, "tile")  # small K would otherwise take the JIT kernel
     env = {"steps2": {"SPCV_STEPS": "2"}, "steps4": {"SPCV_STEPS": "4"}, "nf2": {"SPCV_NF": "2"},
            "nf4_steps2": {"SPCV_NF": "4", "SPCV_STEPS": "2"}}.get(layout, {})
     for k, v in env.items():
@@ -707,7 +718,7 @@ def test_dense_baseline_validation_order():
 
 
 # ------------------------------- executor pointwise step on device (§8f-2)
-@pytest.mark.parametrize("kernel", ["jit", "tile"])
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("hw", [(7, 9), (8, 8)], ids=["odd_spatial", "vec"])
 @pytest.mark.parametrize("bh", [2, 4])
 def test_spmm_layer_padded_rows_and_residual(oracle, monkeypatch, hw, bh, kernel):
@@ -730,9 +741,9 @@ def test_spmm_layer_padded_rows_and_residual(oracle, monkeypatch, hw, bh, kernel
     res = rng.uniform(-1, 1, (B, rows, H, W)).astype(np.float32)
     want = oracle.spmm(m, act, np.r_[bias, np.zeros(pad, np.float32)], RELU6)[:, :rows].reshape(B, rows, H, W)
     want_res = (want + res).astype(np.float32)
-    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    use_kernel(monkeypatch, kernel)
     dw = sp.DeviceBcsr(m)
-    assert dw.kernel() == kernel
+    assert dw.kernel_for(B, H, W) == kernel
     a = torch.from_numpy(act).cuda()
     o = torch.full((B, rows, H, W), float("nan"), device="cuda")
     sp.spmm_layer(dw, a, torch.from_numpy(bias).cuda(), RELU6, o)
@@ -803,14 +814,14 @@ def test_jit_variants_compile_concurrently(oracle):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("kernel", ["jit", "tile"])
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_signed_zeros_and_padding_are_bit_exact(oracle, monkeypatch, kernel):
     """-0.0 biases, -0.0 stored weights, zero activations of both signs and a
     clamp at lo = -0.0: the order of additions decides the sign of zero
     results, and every kernel must reproduce the reference bit for bit."""
     import torch
 
-    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    use_kernel(monkeypatch, kernel)
     rng = np.random.default_rng(17)
     K, M, H, W = 24, 16, 4, 4
     dense = np.zeros((M, K), np.float32)
@@ -827,13 +838,13 @@ def test_signed_zeros_and_padding_are_bit_exact(oracle, monkeypatch, kernel):
         assert np.array_equal(bits(got), bits(want)), fused
 
 
-@pytest.mark.parametrize("kernel", ["jit", "tile"])
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_randomized_shapes_bit_exact(oracle, monkeypatch, kernel):
     """Seeded random layers (K 1..200, M 1..96, block heights 1/2/4, odd and
     even spatial sizes, 1-3 images, 0-99 % sparsity, bias or none, clamp or
     none) through spcv_cu_spmm_into: bit-exact against the oracle for both the
     weight-specialised and the tile kernel."""
-    monkeypatch.setenv("SPCV_JIT", "1" if kernel == "jit" else "0")
+    use_kernel(monkeypatch, kernel)
     monkeypatch.setenv("SPCV_JIT_MAX_SEGS", "48")
     rng = np.random.default_rng(2024)
     for case in range(14):
@@ -867,7 +878,7 @@ def test_tail_and_row_splits_bit_exact(oracle, monkeypatch, env, case):
     """The partial last round of tiles split 2/4/8 ways by rows (tail split),
     every tile split across CTAs (SPCV_SPLIT), other CTA sizes: the LPT bins
     each CTA takes change, the per-row arithmetic does not (bit-exact)."""
-    monkeypatch.setenv("SPCV_JIT", "0")
+    use_kernel(monkeypatch, "tile")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _, layer, images = case
@@ -886,7 +897,7 @@ def test_autotuned_tail_split_bit_exact_and_uncounted(oracle, monkeypatch, case)
     tuned_tail): its result, the cached choice on later calls and the untuned
     heuristic (SPCV_AUTOTUNE=0) are bit-identical to the oracle, and each call
     counts as one launch (the tuning launches are internal)."""
-    monkeypatch.setenv("SPCV_JIT", "0")
+    use_kernel(monkeypatch, "tile")
     _, layer, images = case
     d = make_layer_data(layer, images, 7)
     want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8)
@@ -923,3 +934,44 @@ def test_wide_spmm_layer_padded_rows_and_residual(oracle, hw):
                   residual=torch.from_numpy(res).cuda())
     torch.cuda.synchronize()
     assert np.array_equal(bits(o.cpu().numpy()), bits((want + res).astype(np.float32)))
+
+
+# ------------------------- every kernel on BASELINE-shaped layers (round 2)
+@pytest.mark.parametrize("kernel", ["tile", "small"])
+@pytest.mark.parametrize("case", [
+    ("c1", CONFIGS["c1"]["layers"]()[0], 1),
+    ("c3_b4", Layer("c3_b4", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.9, 4), 6),
+    ("c3_b2", Layer("c3_b2", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.8, 2), 6),
+    ("pw7", mbv1_pointwise()[6], 12),
+    ("pw13", mbv1_pointwise()[12], 12),
+    ("c5_s98", Layer("c5", 1024, 1024, 7, 7, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.98, 1, True), 8),
+], ids=lambda c: c[0])
+def test_kernels_on_config_layers_bit_exact(oracle, monkeypatch, kernel, case):
+    """The tile kernel and the few-column kernel on the BASELINE layer shapes
+    (either forced by the pack-time knobs, whatever the column count) equal
+    the oracle bit for bit, and kernel_for names the kernel that ran."""
+    use_kernel(monkeypatch, kernel)
+    _, layer, images = case
+    d = make_layer_data(layer, images, 31)
+    dw = sp.DeviceBcsr(d.weights)
+    assert dw.kernel_for(images, layer.h, layer.w) == kernel
+    got = run_device(d.weights, d.act, d.bias, layer.act, dw=dw)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8).reshape(got.shape)
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_default_kernel_choice_by_column_count():
+    """Production choice (no knobs): a single c1 image or one MBv1 batch-1
+    layer has fewer column tiles than SMs and runs the few-column kernel; c3 at
+    64 images and MBv1 pw13 at 256 images run the tile kernel."""
+    c1 = CONFIGS["c1"]["layers"]()[0]
+    d = make_layer_data(c1, 1, 3)
+    assert sp.DeviceBcsr(d.weights).kernel_for(1, 28, 28) == "small"
+    p7 = mbv1_pointwise()[6]
+    assert sp.DeviceBcsr(make_layer_data(p7, 1, 3).weights).kernel_for(1, 14, 14) == "small"
+    c3 = Layer("c3", 512, 512, 14, 14, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.9, 4)
+    d3 = make_layer_data(c3, 1, 3)
+    assert sp.DeviceBcsr(d3.weights).kernel_for(64, 14, 14) == "tile"
+    p13 = mbv1_pointwise()[12]
+    d13 = make_layer_data(p13, 1, 3)
+    assert sp.DeviceBcsr(d13.weights).kernel_for(256, 7, 7) == "tile"
