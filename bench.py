@@ -338,8 +338,9 @@ def main():
                               us=us, gflops=d.flops() / us / 1e3, gbs=d.alg_bytes() / us / 1e3,
                               hbm_frac=d.alg_bytes() / us / 1e3 / hbm_peak,
                               alg_bytes=d.alg_bytes(), flops=d.flops(),
-                              kernel=("spcv_jit" if dev_layers[li][0].kernel(args.mode == "strict") == "jit"
-                                      else "spmm_bcsr_kernel")))
+                              kernel={"jit": "spcv_jit", "small": "spmm_small_kernel"}.get(
+                                  dev_layers[li][0].kernel_for(images, d.layer.h, d.layer.w, args.mode == "strict"),
+                                  "spmm_bcsr_kernel")))
     tot_us = sum(p["us"] for p in per_layer)
     for p in per_layer:
         p["share"] = p["us"] / tot_us

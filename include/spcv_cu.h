@@ -107,9 +107,10 @@ int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel);
  * tensors, bias, clamp) runs, which also depends on the column count:
  *   SPCV_KERNEL_JIT     — as above (the k-major variant only with enough
  *                         column groups for its persistent CTAs);
- *   SPCV_KERNEL_SMALL   — fewer column tiles than SMs (batch 1, small planes):
- *                         one warp per block row x 32 columns, activations
- *                         gathered from global memory, no staging (small.cu);
+ *   SPCV_KERNEL_SMALL   — fewer column tiles than SMs and <= 8 M products
+ *                         (batch 1, small planes): one warp per block row x
+ *                         32 columns, activations gathered from global
+ *                         memory, no staging (small.cu);
  *   SPCV_KERNEL_TILE    — everything else.
  * All are bit-exact in SPCV_MODE_STRICT. SPCV_SMALL=0|2 at pack time
  * disables / forces the few-column kernel. Compiles the JIT

@@ -695,8 +695,9 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
 //    kernels' finer work units win — measured: c1, 784 columns, 24 vs 17 us;
 //    MBv2 384->64 @14x14 x128, 25088 columns in 2 segments, 53 vs 38 us);
 //    decided from the plan, so a variant that would not run is never compiled;
-//  * SMALL — fewer column tiles than SMs (batch 1, small planes): a warp per
-//    block row x 32 columns, gathers from global memory (small.cu);
+//  * SMALL — fewer column tiles than SMs and at most kSmallMaxProducts
+//    products (batch 1, small planes): a warp per block row x 32 columns,
+//    gathers from global memory (small.cu);
 //  * TILE — everything else (any K, any layout, channel passes).
 int pick_kernel(const spcv_cu_weights* w, long long N, long long S, long long ntiles, int sms, bool vec, bool pass,
                 bool strict, bool clamp, bool has_bias, const float* residual, uintptr_t act, uintptr_t out,
@@ -723,7 +724,11 @@ int pick_kernel(const spcv_cu_weights* w, long long N, long long S, long long nt
             }
         }
     }
-    if (!pass && kn.small && w->d_row_ptr && w->brows <= 65535 * 4 && (kn.small > 1 || ntiles < sms))
+    // (products bound: the few-column kernel gathers through L1/L2 without
+    // reuse; beyond a few million products the staged tiles win — measured:
+    // MBv2 160->960 @7x7 x128, 144 M products, 133 vs 53 us)
+    if (!pass && kn.small && w->d_row_ptr && w->brows <= 65535 * 4 &&
+        (kn.small > 1 || (ntiles < sms && static_cast<double>(w->nblocks) * w->block_h * N <= kSmallMaxProducts)))
         return SPCV_KERNEL_SMALL;
     return SPCV_KERNEL_TILE;
 }

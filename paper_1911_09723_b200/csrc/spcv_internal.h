@@ -151,6 +151,7 @@ int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
 // Few-column kernel (small.cu): one warp per block row x 32 columns, gathers
 // straight from global memory. SPCV_ERR_UNSUPPORTED when it cannot serve.
 int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& a, bool strict, cudaStream_t st);
+constexpr double kSmallMaxProducts = 8.0e6;  // products (stored values x columns) per call
 
 // Weight-specialised kernels (jit.cu): one persistent CTA of kJitWarps warps
 // per SM, a kJitStages-deep ring of [32 channels][64 columns] fp32 per warp.

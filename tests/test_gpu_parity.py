@@ -960,10 +960,11 @@ def test_kernels_on_config_layers_bit_exact(oracle, monkeypatch, kernel, case):
     assert np.array_equal(bits(got), bits(want))
 
 
-def test_default_kernel_choice_by_column_count():
+def test_default_kernel_choice_by_column_count(monkeypatch):
     """Production choice (no knobs): a single c1 image or one MBv1 batch-1
     layer has fewer column tiles than SMs and runs the few-column kernel; c3 at
     64 images and MBv1 pw13 at 256 images run the tile kernel."""
+    monkeypatch.delenv("SPCV_JIT_KMAJOR_MIN_COLS", raising=False)  # production threshold (conftest sets 0)
     c1 = CONFIGS["c1"]["layers"]()[0]
     d = make_layer_data(c1, 1, 3)
     assert sp.DeviceBcsr(d.weights).kernel_for(1, 28, 28) == "small"

@@ -116,7 +116,7 @@ def main():
                     parity = "n/a (fast)"
                 rows.append({"layer": L.name, "K": L.cin, "M": L.cout, "S": L.spatial, "bh": L.block_h,
                              "sparsity": L.sparsity, "images": images, "nnz": d.nnz,
-                             "kernel": dw.kernel(args.mode == "strict"),
+                             "kernel": dw.kernel_for(images, L.h, L.w, args.mode == "strict"),
                              "cold_us": times["cold"], "warm_us": times["warm"],
                              "flops": d.flops(), "alg_bytes": d.alg_bytes(), "parity": parity})
         f_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6

@@ -29,7 +29,17 @@ def main():
     ap.add_argument("--mode", choices=["strict", "fast"], default="strict")
     ap.add_argument("--check", type=int, default=0,
                     help="compare the first N images with the CPU oracle (strict: bit-exact)")
+    ap.add_argument("--adhoc", default=None,
+                    help="K,M,H,W,sparsity,block_h,images: a synthetic layer instead of a config layer")
     args = ap.parse_args()
+    if args.adhoc:
+        from paper_1911_09723_b200.workloads import Layer
+        K, M, H, W, sp_, bh, images = args.adhoc.split(",")
+        L = Layer("adhoc", int(K), int(M), int(H), int(W), ("clamp", 0.0, float("inf")), -1.0, 1.0,
+                  float(sp_), int(bh))
+        args.images = int(images)
+        run_layer(args, {"images": int(images)}, 0, L, "adhoc")
+        return
     cfg = CONFIGS[args.config]
     layers = {L.name: (i, L) for i, L in enumerate(cfg["layers"]())}
     for name in args.layer.split(","):
@@ -42,7 +52,7 @@ def run_layer(args, cfg, li, L, name):
     dw = sp.DeviceBcsr(d.weights)
     import time
     t0 = time.time()
-    kern = dw.kernel(args.mode == "strict")
+    kern = dw.kernel_for(images, L.h, L.w, args.mode == "strict")
     prep = time.time() - t0
     a = torch.from_numpy(d.act).cuda()
     b = torch.from_numpy(d.bias).cuda()
