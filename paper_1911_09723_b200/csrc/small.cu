@@ -5,7 +5,8 @@
 // batch-1 MobileNet stack) there are fewer tiles than SMs and every CTA pays
 // its staging / ring-fill / epilogue latency once for little work. Here one
 // warp owns one block row x 32 virtual columns (lane = column): it reads the
-// row's stored blocks once (coalesced, 32 at a time, then broadcast with
+// row's stored blocks once (coalesced, 32 at a time — the first 32 from a
+// per-row head table, so they do not wait for row_ptr — then broadcast with
 // shuffles) and gathers each block's activation straight from global memory
 // (one coalesced 128 B row segment per block, L1/L2-resident at these sizes).
 // There is no shared-memory staging and no CTA barrier, and the grid has
@@ -29,6 +30,8 @@ struct SmallArgs {
     const uint32_t* row_ptr;  // [brows + 1]
     const uint32_t* col_idx;  // [nblocks]
     const float* values;      // [nblocks][BH]
+    const uint32_t* head_col; // [brows][32]: each block row's first 32 column indices (~0u past its end)
+    const float* head_val;    // [brows][32][BH]: their values (0 past the end)
     long long N;              // images * S
     int S, K_img, M_out, brows;
     int act_kind;
@@ -68,14 +71,17 @@ spmm_small_kernel(const SmallArgs a) {
         const int r = br * BH + i;
         acc[i] = (a.bias != nullptr && r < a.M_out) ? __ldg(a.bias + r) : 0.0f;
     }
-    const uint32_t rb = __ldg(a.row_ptr + br), re = __ldg(a.row_ptr + br + 1);
-    for (uint32_t t0 = rb; t0 < re; t0 += 32) {
-        const uint32_t cnt = min(32u, re - t0);
-        const bool mine = static_cast<uint32_t>(lane) < cnt;
-        const uint32_t kcol = mine ? __ldg(a.col_idx + t0 + lane) : 0u;
-        float wv[BH];
+    // The row's first 32 blocks come from the head table (no dependency on
+    // row_ptr, loaded in the same round trip); later groups of 32 from
+    // col_idx / values at row_ptr[br] + 32.
+    const size_t h = static_cast<size_t>(br) * 32 + lane;
+    uint32_t kcol = __ldg(a.head_col + h);
+    float wv[BH];
 #pragma unroll
-        for (int i = 0; i < BH; ++i) wv[i] = mine ? __ldg(a.values + static_cast<size_t>(t0 + lane) * BH + i) : 0.0f;
+    for (int i = 0; i < BH; ++i) wv[i] = __ldg(a.head_val + h * BH + i);
+    const uint32_t rb = __ldg(a.row_ptr + br), re = __ldg(a.row_ptr + br + 1);
+    for (uint32_t t0 = rb;;) {
+        const uint32_t cnt = min(32u, re - t0);
         // 8 gathers in flight, then their products, in stored order
         for (uint32_t t = 0; t < cnt; t += 8) {
             float x[8];
@@ -93,6 +99,12 @@ spmm_small_kernel(const SmallArgs a) {
                 }
             }
         }
+        t0 += 32;
+        if (t0 >= re) break;
+        const bool mine = t0 + lane < re;
+        kcol = mine ? __ldg(a.col_idx + t0 + lane) : 0u;
+#pragma unroll
+        for (int i = 0; i < BH; ++i) wv[i] = mine ? __ldg(a.values + static_cast<size_t>(t0 + lane) * BH + i) : 0.0f;
     }
     if (!valid) return;
 #pragma unroll
@@ -128,7 +140,7 @@ static int launch_small_bh(const spcvk::SmallArgs& a, bool strict, cudaStream_t 
 }
 
 int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& k, bool strict, cudaStream_t st) {
-    if (!w->d_row_ptr || !w->d_col_idx) return SPCV_ERR_UNSUPPORTED;
+    if (!w->d_row_ptr || !w->d_col_idx || !w->d_head_col) return SPCV_ERR_UNSUPPORTED;
     if ((k.N + 31) / 32 > 0x7FFFFFFFLL || w->brows > 65535 * spcvk::kSmallWarps) return SPCV_ERR_UNSUPPORTED;
     spcvk::SmallArgs a;
     a.act = k.act;
@@ -138,6 +150,8 @@ int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& k, bool stri
     a.row_ptr = w->d_row_ptr;
     a.col_idx = w->d_col_idx;
     a.values = w->d_values;
+    a.head_col = w->d_head_col;
+    a.head_val = w->d_head_val;
     a.N = k.N;
     a.S = k.S;
     a.K_img = k.K_img;

@@ -171,6 +171,8 @@ void free_weights(spcv_cu_weights* w) {
     cudaFree(w->d_bin_beg_fast);
     cudaFree(w->d_row_ptr);
     cudaFree(w->d_col_idx);
+    cudaFree(w->d_head_col);
+    cudaFree(w->d_head_val);
     for (spcv_cu_weights* p : w->parts) free_weights(p);
     jit_release(w);
     delete w;
@@ -473,8 +475,19 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
             w->h_values.assign(values, values + nvalues);
         }
     }
+    // head table of the few-column kernel: each block row's first 32 blocks
+    std::vector<uint32_t> head_col(static_cast<size_t>(brows) * 32, ~0u);
+    std::vector<float> head_val(static_cast<size_t>(brows) * 32 * BH, 0.0f);
+    for (int r = 0; r < brows; ++r)
+        for (uint32_t b = row_ptr[r], i = 0; b < row_ptr[r + 1] && i < 32; ++b, ++i) {
+            head_col[static_cast<size_t>(r) * 32 + i] = col_idx[b];
+            for (int j = 0; j < BH; ++j)
+                head_val[(static_cast<size_t>(r) * 32 + i) * BH + j] = values[static_cast<size_t>(b) * BH + j];
+        }
     int rc = SPCV_OK;
-    if ((rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
+    if ((rc = upload(&w->d_head_col, head_col.data(), head_col.size())) ||
+        (rc = upload(&w->d_head_val, head_val.data(), head_val.size())) ||
+        (rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
         (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
         (rc = upload(&w->d_values, values, nvalues)) ||
         (rc = upload(&w->d_stream, reinterpret_cast<const uint4*>(bs.stream.data()), bs.stream.size() / 16)) ||

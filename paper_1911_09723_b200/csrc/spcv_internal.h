@@ -105,6 +105,8 @@ struct spcv_cu_weights {
     // plain BCSR row_ptr / col_idx (d_values holds the blocks) for the few-column kernel (small.cu)
     uint32_t* d_row_ptr = nullptr;
     uint32_t* d_col_idx = nullptr;
+    uint32_t* d_head_col = nullptr;  // [brows][32] first 32 column indices per block row (~0u past the end)
+    float* d_head_val = nullptr;     // [brows][32][block_h]
     uint2* d_groups_fast = nullptr;
     int ngroups = 0;
     Knobs knobs;  // tuning knobs at pack time
