@@ -528,14 +528,16 @@ def time_steps(sp, dev_layers, steps, warmup, stream, dist, dev, flush_buf, per_
         launches0 = sp.launch_count()
         with ClockProbe(dev) as clk:
             if flush_buf is None:
-                start, end = ev(), ev()
-                start.record(stream)
-                for _ in range(steps):
+                # back to back; an event at every step boundary gives the per-step
+                # median too (recording an event adds no gap on the stream)
+                marks = [ev() for _ in range(steps + 1)]
+                marks[0].record(stream)
+                for k in range(steps):
                     step()
-                end.record(stream)
+                    marks[k + 1].record(stream)
                 torch.cuda.synchronize()
-                ms_local = start.elapsed_time(end)
-                step_ms = None
+                ms_local = marks[0].elapsed_time(marks[-1])
+                step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(steps)]
             else:
                 pairs = []
                 for _ in range(steps):
@@ -562,9 +564,10 @@ def time_steps(sp, dev_layers, steps, warmup, stream, dist, dev, flush_buf, per_
             per_layer_us = [statistics.mean(lev[k][li][0].elapsed_time(lev[k][li][1]) for k in range(steps)) * 1e3
                             for li in range(nl)]
     ms_total = dist.max(ms_local, device=cdev)
-    timing = {"region": "K back-to-back steps, one event pair" if flush_buf is None else
+    timing = {"region": "K back-to-back steps, events at every step boundary" if flush_buf is None else
               "K steps, one event pair each, L2 overwritten (252 MB fill) between steps",
-              "median_step_ms": round(statistics.median(step_ms), 4) if step_ms else None}
+              "median_step_ms": round(statistics.median(step_ms), 4) if step_ms else None,
+              "value_from": "total time of the K timed steps / K (max over ranks)"}
     return {"ms_step": ms_total / steps, "launches": launches, "clk": clk, "per_layer_us": per_layer_us,
             "timing": timing}
 
@@ -871,6 +874,20 @@ def bench_network(args, dev, stream, dist, batch):
     return out
 
 
+def mapped_libraries() -> list[str]:
+    """Shared objects of this repo (or the reference build) mapped into this
+    process (/proc/self/maps): the reference arm must map oracle/_ref only."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if len(line.split()) >= 6 else ""
+            if path.endswith(".so") and path.startswith(ROOT):
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference(args, layers):
     """--impl reference: the reference's own CPU spmm_into (oracle/_ref, else
     the oracle port) on all host threads over the WHOLE job (the global batch,
@@ -920,7 +937,11 @@ def run_reference(args, layers):
                                    f"over {threads} threads"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_libraries_mapped": mapped_libraries(),
     }
+    if any("libspcv_cu" in p or "libspcv_b200" in p for p in line["repo_libraries_mapped"]):
+        log(f"reference arm mapped this repo's CUDA library: {line['repo_libraries_mapped']}")
+        sys.exit(2)
     print(json.dumps(line), flush=True)
 
 
