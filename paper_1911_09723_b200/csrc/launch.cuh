@@ -24,7 +24,7 @@ struct Geometry {
 };
 
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref);
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref);
 
 template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
@@ -44,9 +44,10 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     // knobs: cache the last one.
     static thread_local long long key[7] = {-1, -1, -1, -1, -1, -1, -2};
     static thread_local Geometry g;
-    const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, w->knobs.geometry_key(), a.tail_pref};
+    const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, w->knobs.geometry_key(),
+                            a.tail_pref * 64LL + a.split_pref};
     if (!std::equal(k, k + 7, key)) {
-        g = geometry(kern, w, ntiles, sms, a.tail_pref);
+        g = geometry(kern, w, ntiles, sms, a.tail_pref, a.split_pref);
         std::copy(k, k + 7, key);
     }
     dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
@@ -120,7 +121,7 @@ int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt
 // each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
 // split tiles across CTAs (row split) until the grid covers the GPU.
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref) {
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref) {
     Geometry g;
     g.ntiles = ntiles;
     g.smem = smem_bytes(w->cols, w->rows, w->T);
@@ -142,6 +143,8 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
     g.split = 1;
     while (g.nwarps * g.split * 2 <= kBins && ntiles * g.split < static_cast<long long>(sms) * per_sm)
         g.split *= 2;
+    if (split_pref > 0 && g.nwarps * split_pref <= kBins && (split_pref & (split_pref - 1)) == 0)
+        g.split = split_pref;  // autotuned (spcv_cu.cu)
     if (kn.split) {
         const int want = kn.split;
         if (want >= 1 && g.nwarps * want <= kBins && (want & (want - 1)) == 0) g.split = want;

@@ -641,47 +641,60 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
     return SPCV_OK;
 }
 
-// Autotuned tail split. The last, partial round of column tiles can run
-// unsplit or split 2 or 4 ways by rows; which is fastest depends on the
-// layer (measured: c3 at 2-3 tiles per SM 7 % faster unsplit, MBv1 pw12 at
-// the same tile count 25 % slower), and every choice gives the same bits (the
-// per-row arithmetic does not depend on the split). The first call of a
-// (weights, columns, mode, layout) shape times the candidates with events on
-// its stream (two launches each after one warm-up) and caches the winner in
-// the weights. Not tuned (heuristic) when SPCV_AUTOTUNE=0 or SPCV_TAIL is set;
-// a shape first seen with an output overlapping its residual (a repeated
-// launch would re-add it) or inside a stream capture uses the heuristic until
-// an eligible call has tuned it.
+// Autotuned launch geometry. The last, partial round of column tiles can run
+// unsplit or split 2 or 4 ways by rows; with few tiles (fewer than two per SM:
+// small batches, the per-GPU shards of a batch partitioned over GPUs) the
+// number of CTAs sharing every tile (row split) matters too. Which is fastest
+// depends on the layer (measured: c3 at 2-3 tiles per SM 7 % faster unsplit,
+// MBv1 pw12 at the same tile count 25 % slower; MBv1 at 32 images per GPU the
+// best row split differs per layer, 9 % over the heuristic), and every choice
+// gives the same bits (the per-row arithmetic does not depend on the split).
+// The first call of a (weights, columns, mode, layout) shape times the
+// candidates with events on its stream (two launches each after one warm-up)
+// and caches the winner in the weights. Not tuned (heuristic) when
+// SPCV_AUTOTUNE=0 or SPCV_TAIL is set; a shape first seen with an output
+// overlapping its residual (a repeated launch would re-add it) or inside a
+// stream capture uses the heuristic until an eligible call has tuned it.
+struct TunedGeometry {
+    int tail = -1;   // -1: heuristic
+    int split = 0;   // 0: heuristic
+};
+
 template <typename Run>
-int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, bool strict, bool vec,
-               cudaStream_t st, Run&& run) {
-    if (!w->knobs.autotune || w->knobs.tail >= 0) return -1;
+TunedGeometry tuned_geometry(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, long long ntiles,
+                             int sms, bool strict, bool vec, cudaStream_t st, Run&& run) {
+    TunedGeometry none;
+    if (!w->knobs.autotune || w->knobs.tail >= 0) return none;
     const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
     {
         std::lock_guard<std::mutex> lk(w->tune_mu);
         for (const auto& kv : w->tuned_tail)
-            if (kv.first == key) return kv.second;  // also inside a capture / with a residual
+            if (kv.first == key) return TunedGeometry{kv.second % 64 - 1, kv.second / 64};  // also inside a capture
     }
-    if (a.acc_in) return -1;  // a later channel pass reads out: not repeatable in place
+    if (a.acc_in) return none;  // a later channel pass reads out: not repeatable in place
     if (a.residual) {  // repeated launches are idempotent unless out overlaps the residual
         const size_t bytes = static_cast<size_t>(N / a.S) * a.M_out * a.S * sizeof(float);
         const char* r0 = reinterpret_cast<const char*>(a.residual);
         const char* o0 = reinterpret_cast<const char*>(a.out);
-        if (r0 < o0 + bytes && o0 < r0 + bytes) return -1;
+        if (r0 < o0 + bytes && o0 < r0 + bytes) return none;
     }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return -1;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return none;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
         if (e0) cudaEventDestroy(e0);
-        return -1;
+        return none;
     }
-    int best = -1;
+    std::vector<TunedGeometry> cands = {{-1, 0}, {0, 0}, {2, 0}, {4, 0}};
+    if (ntiles < 2LL * sms && w->knobs.split == 0)  // few tiles: the row split too
+        for (int sp : {1, 2, 4, 8}) cands.push_back(TunedGeometry{-1, sp});
+    TunedGeometry best;
     float best_ms = 0.0f;
     uint64_t runs = 0;  // tuning launches are not the caller's work: not counted
-    for (int cand : {-1, 0, 2, 4}) {
+    for (const TunedGeometry& cand : cands) {
         spcvk::KernelArgs t = a;
-        t.tail_pref = cand;
+        t.tail_pref = cand.tail;
+        t.split_pref = cand.split;
         if (run(t) != SPCV_OK) continue;  // warm-up (geometry, L2)
         ++runs;
         cudaEventRecord(e0, st);
@@ -698,7 +711,7 @@ int tuned_tail(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N
     cudaEventDestroy(e1);
     g_launches.fetch_sub(runs, std::memory_order_relaxed);
     std::lock_guard<std::mutex> lk(w->tune_mu);
-    w->tuned_tail.emplace_back(key, best);
+    w->tuned_tail.emplace_back(key, best.split * 64 + best.tail + 1);
     return best;
 }
 
@@ -798,6 +811,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.tail_start = 0x7FFFFFFFFFFFFFFFLL;
     a.tail_split = 1;
     a.tail_pref = -1;
+    a.split_pref = 0;
     a.one2 = 0x3f8000003f800000ULL;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
@@ -827,7 +841,9 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
             default: return launch_bh4(args, w, ntiles, sms, strict, vec, st);
         }
     };
-    a.tail_pref = tuned_tail(w, a, N, strict, vec, st, run);
+    const TunedGeometry tg = tuned_geometry(w, a, N, ntiles, sms, strict, vec, st, run);
+    a.tail_pref = tg.tail;
+    a.split_pref = tg.split;
     return run(a);
 }
 

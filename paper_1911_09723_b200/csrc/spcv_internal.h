@@ -121,7 +121,7 @@ struct spcv_cu_weights {
     // channel order, each continuing the previous part's sums (spcv_cu.cu)
     std::vector<spcv_cu_weights*> parts;
     std::vector<int> part_k0;
-    // autotuned tail split per call shape (spcv_cu.cu: tuned_tail)
+    // autotuned launch geometry per call shape: split * 64 + tail + 1 (spcv_cu.cu: tuned_geometry)
     mutable std::mutex tune_mu;
     mutable std::vector<std::pair<long long, int>> tuned_tail;
 };

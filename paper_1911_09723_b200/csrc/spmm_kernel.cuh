@@ -65,6 +65,7 @@ struct KernelArgs {
     int tail_split;
     int steps;               // steps per chunk of `stream` (host-side dispatch)
     int tail_pref;           // host-side: tail split chosen by the autotuner (-1: heuristic, 0: none)
+    int split_pref;          // host-side: CTAs per tile chosen by the autotuner (0: heuristic)
     // {1.0f, 1.0f} as f32x2, passed at run time so ptxas cannot fold the
     // strict pair mul.rn.f32x2 + fma.rn.f32x2(acc, one, p) into one FFMA2.
     unsigned long long one2;

@@ -71,7 +71,21 @@ def main():
     orc = bench._oracle()
     oracle = orc.Oracle()
     threads = os.cpu_count() or 1
+    # floor of this timing method: an empty-ish launch (a 4-byte fill) measured the same way
+    tiny = torch.zeros(1, device="cuda")
+    floor = []
+    with torch.cuda.stream(stream):
+        for _ in range(REPS):
+            torch.cuda._sleep(GATE_CYCLES)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tiny.fill_(1.0)
+            e1.record(stream)
+            floor.append((e0, e1))
+        stream.synchronize()
+    floor_us = statistics.median(e0.elapsed_time(e1) * 1e3 for e0, e1 in floor)
     results = {"hbm_gbs": hbm, "peak_kind": peak_kind, "sms": sms, "configs": {},
+               "timing_floor_us": floor_us,
                "cpu": {"model": bench.cpu_model(), "cores": threads,
                        "kind": "reference" if orc.have_ref() else "port"}}
     for cname in args.configs.split(","):
@@ -171,6 +185,9 @@ def markdown(res) -> str:
                        f"{r['cold_us']:.1f} / {r['warm_us']:.1f} | {r['cold_gflops']:.0f} | {r['cold_gbs']:.0f} | "
                        f"{100 * r['cold_hbm_frac']:.1f} | {r['binding']} ({r['t_bound_us']:.1f}) | "
                        f"{100 * r['cold_frac_of_bound']:.0f} | {r['parity']} | {r['kernel']} |")
+    out.append("")
+    out.append(f"Timing floor of this method (a 4-byte fill kernel timed the same way): "
+               f"{res.get('timing_floor_us', float('nan')):.1f} µs; CUDA event resolution on this GPU is 2.048 µs.")
     out.append("")
     out.append(f"CPU = the reference `spmm_into` (oracle/_ref, {res['cpu']['kind']}) on "
                f"{res['cpu']['model']} ({res['cpu']['cores']} threads).")
