@@ -54,7 +54,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
 spmm_small_kernel(const SmallArgs a) {
     const int lane = threadIdx.x & 31;
     const int br = blockIdx.y * kSmallWarps + (threadIdx.x >> 5);
-    if (br >= a.brows) return;
+    if (br >= a.brows) {
+        pdl_trigger();
+        return;
+    }
     const long long n = static_cast<long long>(blockIdx.x) * 32 + lane;
     const bool valid = n < a.N;
     long long abase = 0, obase = 0;
@@ -65,12 +68,7 @@ spmm_small_kernel(const SmallArgs a) {
         obase = img * a.M_out * a.S + s;
     }
     const float* act = a.act + abase;
-    float acc[BH];
-#pragma unroll
-    for (int i = 0; i < BH; ++i) {
-        const int r = br * BH + i;
-        acc[i] = (a.bias != nullptr && r < a.M_out) ? __ldg(a.bias + r) : 0.0f;
-    }
+    pdl_trigger();
     // The row's first 32 blocks come from the head table (no dependency on
     // row_ptr, loaded in the same round trip); later groups of 32 from
     // col_idx / values at row_ptr[br] + 32.
@@ -80,6 +78,13 @@ spmm_small_kernel(const SmallArgs a) {
 #pragma unroll
     for (int i = 0; i < BH; ++i) wv[i] = __ldg(a.head_val + h * BH + i);
     const uint32_t rb = __ldg(a.row_ptr + br), re = __ldg(a.row_ptr + br + 1);
+    pdl_wait();  // activations, bias and residual may come from the previous kernel on the stream
+    float acc[BH];
+#pragma unroll
+    for (int i = 0; i < BH; ++i) {
+        const int r = br * BH + i;
+        acc[i] = (a.bias != nullptr && r < a.M_out) ? __ldg(a.bias + r) : 0.0f;
+    }
     for (uint32_t t0 = rb;;) {
         const uint32_t cnt = min(32u, re - t0);
         // 8 gathers in flight, then their products, in stored order
@@ -124,17 +129,13 @@ spmm_small_kernel(const SmallArgs a) {
 namespace spcv_detail {
 
 template <int BH>
-static int launch_small_bh(const spcvk::SmallArgs& a, bool strict, cudaStream_t st) {
+static int launch_small_bh(const spcvk::SmallArgs& a, bool strict, bool pdl, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((a.N + 31) / 32),
                     static_cast<unsigned>((a.brows + spcvk::kSmallWarps - 1) / spcvk::kSmallWarps));
-    const int threads = spcvk::kSmallWarps * 32;
-    if (strict)
-        a.residual ? spcvk::spmm_small_kernel<BH, true, true><<<grid, threads, 0, st>>>(a)
-                   : spcvk::spmm_small_kernel<BH, true, false><<<grid, threads, 0, st>>>(a);
-    else
-        a.residual ? spcvk::spmm_small_kernel<BH, false, true><<<grid, threads, 0, st>>>(a)
-                   : spcvk::spmm_small_kernel<BH, false, false><<<grid, threads, 0, st>>>(a);
-    SPCV_CUDA(cudaGetLastError());
+    const dim3 threads(spcvk::kSmallWarps * 32);
+    auto kern = strict ? (a.residual ? spcvk::spmm_small_kernel<BH, true, true> : spcvk::spmm_small_kernel<BH, true, false>)
+                       : (a.residual ? spcvk::spmm_small_kernel<BH, false, true> : spcvk::spmm_small_kernel<BH, false, false>);
+    SPCV_CUDA(launch_kernel(kern, grid, threads, 0, st, pdl, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }
@@ -161,9 +162,9 @@ int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& k, bool stri
     a.lo = k.lo;
     a.hi = k.hi;
     switch (w->block_h) {
-        case 1: return launch_small_bh<1>(a, strict, st);
-        case 2: return launch_small_bh<2>(a, strict, st);
-        default: return launch_small_bh<4>(a, strict, st);
+        case 1: return launch_small_bh<1>(a, strict, k.pdl, st);
+        case 2: return launch_small_bh<2>(a, strict, k.pdl, st);
+        default: return launch_small_bh<4>(a, strict, k.pdl, st);
     }
 }
 

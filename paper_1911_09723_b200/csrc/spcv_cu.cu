@@ -67,6 +67,7 @@ Knobs Knobs::from_env() {
     k.jit_interleave = static_cast<int>(get("SPCV_JIT_INTERLEAVE", 1));
     k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
     k.small = static_cast<int>(get("SPCV_SMALL", 1));
+    k.pdl = static_cast<int>(get("SPCV_PDL", 1));
     return k;
 }
 
@@ -812,6 +813,8 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.tail_split = 1;
     a.tail_pref = -1;
     a.split_pref = 0;
+    a.pdl = w->knobs.pdl > 1 ||
+            (w->knobs.pdl == 1 && static_cast<double>(w->nblocks) * w->block_h * N <= kPdlMaxProducts);
     a.one2 = 0x3f8000003f800000ULL;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
@@ -827,7 +830,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                                  reinterpret_cast<uintptr_t>(act), reinterpret_cast<uintptr_t>(out), a.M_out, &jv);
     if (kind == SPCV_KERNEL_JIT) {
         // A failed compile (recorded, never retried) falls back to the other kernels.
-        if (const JitVariant* v = jit_build(w, jv)) return jit_launch(v, a, st);
+        if (const JitVariant* v = jit_build(w, jv)) return jit_launch(v, a, st, nullptr, a.pdl);
     }
     if (kind == SPCV_KERNEL_SMALL) {
         const int rc = launch_small(w, a, strict, st);

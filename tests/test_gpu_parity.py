@@ -976,3 +976,45 @@ def test_default_kernel_choice_by_column_count(monkeypatch):
     p13 = mbv1_pointwise()[12]
     d13 = make_layer_data(p13, 1, 3)
     assert sp.DeviceBcsr(d13.weights).kernel_for(256, 7, 7) == "tile"
+
+
+@pytest.mark.parametrize("pdl", ["2", "0"])
+def test_chained_layers_on_one_stream_bit_exact(oracle, monkeypatch, pdl):
+    """Layers launched back to back on one stream, each consuming the previous
+    layer's output and overwriting a buffer an earlier layer read, across the
+    three kernels (weight-specialised, tile, few-column): with programmatic
+    dependent launch (SPCV_PDL=2: always; the default uses it for short calls) every kernel waits for its
+    predecessor before reading its input or writing its output, so the chain
+    equals the oracle applied layer by layer, bit for bit."""
+    import torch
+
+    monkeypatch.setenv("SPCV_PDL", pdl)
+    rng = np.random.default_rng(77)
+    chans = [48, 64, 96, 96, 128, 64, 32]  # K=48 (JIT direct), larger K (tile / few-column)
+    H = W = 14
+    B = 8
+    mats, biases = [], []
+    for k, m in zip(chans[:-1], chans[1:]):
+        d = (rng.standard_normal((m, k)) * 0.2).astype(np.float32)
+        d[rng.random((m, k)) < 0.8] = 0
+        mats.append(sp.encode_bcsr(d, 1))
+        biases.append(rng.uniform(-0.5, 0.5, m).astype(np.float32))
+    x = rng.uniform(-1, 1, (B, chans[0], H, W)).astype(np.float32)
+    want = x
+    for m, b in zip(mats, biases):
+        want = oracle.spmm(m, want, b, RELU6).reshape(B, -1, H, W)
+    dws = [sp.DeviceBcsr(m) for m in mats]
+    # ping-pong buffers: layer i writes the buffer layer i-1 read from
+    bufs = [torch.empty(B * max(chans) * H * W, device="cuda") for _ in range(2)]
+    cur = bufs[0][: x.size].view(x.shape)
+    cur.copy_(torch.from_numpy(x))
+    s = torch.cuda.Stream()
+    kinds = set()
+    with torch.cuda.stream(s):
+        for i, (dw, b) in enumerate(zip(dws, biases)):
+            kinds.add(dw.kernel_for(B, H, W))
+            out = bufs[(i + 1) % 2][: B * chans[i + 1] * H * W].view(B, chans[i + 1], H, W)
+            sp.spmm_batched_into(dw, cur, torch.from_numpy(b).cuda(), RELU6, out, stream=s)
+            cur = out
+        s.synchronize()
+    assert np.array_equal(bits(cur.cpu().numpy()), bits(want))
