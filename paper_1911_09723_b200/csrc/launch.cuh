@@ -24,12 +24,13 @@ struct Geometry {
 };
 
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref);
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref,
+                  int max_threads);
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                  cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC, CAP>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -47,7 +48,7 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, w->knobs.geometry_key(),
                             a.tail_pref * 64LL + a.split_pref};
     if (!std::equal(k, k + 7, key)) {
-        g = geometry(kern, w, ntiles, sms, a.tail_pref, a.split_pref);
+        g = geometry(kern, w, ntiles, sms, a.tail_pref, a.split_pref, CAP ? spcvk::kCapThreads : spcvk::kThreads);
         std::copy(k, k + 7, key);
     }
     dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
@@ -72,6 +73,15 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
                               : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false, true>(a, w, ntiles, sms, st);
         else
             return fail(SPCV_ERR_UNSUPPORTED, "spmm: channel pass with an unexpected layout");
+    }
+    // The register-capped build (three 8-warp CTAs per SM) of the unstructured
+    // 2-step kernels, where three tiles fit in shared memory and the CTA size is free.
+    if constexpr (BH == 1 && STEPS == 2 && VEC && STRICT) {
+        const Knobs& kn = w->knobs;
+        if (kn.regcap && (kn.nwarps == 0 || kn.nwarps <= 8) &&
+            3 * smem_bytes(w->cols, w->rows, w->T) <= kSmemLimit)
+            return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true, false, true>(a, w, ntiles, sms, st)
+                              : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false, false, true>(a, w, ntiles, sms, st);
     }
     return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true>(a, w, ntiles, sms, st)
                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
@@ -120,15 +130,16 @@ int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt
 // each CTA stages its own tile, so more CTAs keep more bytes in flight. Then
 // split tiles across CTAs (row split) until the grid covers the GPU.
 template <typename Kern>
-Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref) {
+Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref,
+                  int max_threads) {
     Geometry g;
     g.ntiles = ntiles;
     g.smem = smem_bytes(w->cols, w->rows, w->T);
     int best = 0, per_sm = 1;
-    g.nwarps = 16;
+    g.nwarps = std::min(16, max_threads / 32);
     const Knobs& kn = w->knobs;
     for (int nw : {4, 8, 16}) {
-        if (nw * 32 > spcvk::kThreads) continue;
+        if (nw * 32 > max_threads) continue;
         if (kn.nwarps && kn.nwarps != nw) continue;
         int ctas = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)

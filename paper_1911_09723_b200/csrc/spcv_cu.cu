@@ -68,6 +68,7 @@ Knobs Knobs::from_env() {
     k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
     k.small = static_cast<int>(get("SPCV_SMALL", 1));
     k.pdl = static_cast<int>(get("SPCV_PDL", 1));
+    k.regcap = get("SPCV_REGCAP", 1) != 0;
     return k;
 }
 

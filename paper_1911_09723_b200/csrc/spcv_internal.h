@@ -35,8 +35,11 @@ struct Knobs {
     int pass_k = 0;        // SPCV_PASS_K: run matrices wider than this as channel passes of this width
     int small = 1;         // SPCV_SMALL: 0 = never the few-column kernel, 2 = always (single pass)
     int pdl = 1;           // SPCV_PDL: programmatic dependent launch 0 = never, 1 = short calls, 2 = always
+    int regcap = 1;        // SPCV_REGCAP=0: never the 80-register build of the unstructured 2-step kernels
     static Knobs from_env();
-    long long geometry_key() const { return (static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1; }
+    long long geometry_key() const {
+        return ((static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1) * 2 + regcap;
+    }
 };
 
 // A weight-specialised kernel compiled at run time (jit.cu), one per call
@@ -100,16 +103,11 @@ struct spcv_cu_weights {
     uint32_t* d_bin_beg = nullptr;
     uint4* d_stream_fast = nullptr;     // null: fast mode shares the strict stream
     uint32_t* d_bin_beg_fast = nullptr;
-    // row groups in LPT order, {first chunk, chunks} of d_stream / d_stream_fast
-    // (the persistent kernel takes them one at a time)
-    uint2* d_groups = nullptr;
     // plain BCSR row_ptr / col_idx (d_values holds the blocks) for the few-column kernel (small.cu)
     uint32_t* d_row_ptr = nullptr;
     uint32_t* d_col_idx = nullptr;
     uint32_t* d_head_col = nullptr;  // [brows][32] first 32 column indices per block row (~0u past the end)
     float* d_head_val = nullptr;     // [brows][32][block_h]
-    uint2* d_groups_fast = nullptr;
-    int ngroups = 0;
     Knobs knobs;  // tuning knobs at pack time
     // small-K path (jit.cu): host copy of the matrix and the planned / compiled
     // variants (a cache inside a const weights object: mutable, guarded by jit.cu's mutex)

@@ -150,6 +150,9 @@ __device__ __forceinline__ float clamp_ref(float v, int kind, float lo, float hi
     if (kind == 1) v = v < lo ? lo : (v > hi ? hi : v);
     return v;
 }
+// Lower bound only: the same ternary when hi = +inf (v > +inf is false for
+// every v, NaN included), i.e. ReLU — half the compare/select instructions.
+__device__ __forceinline__ float clamp_lo(float v, float lo) { return v < lo ? lo : v; }
 
 constexpr uint32_t kNoRow = 0xFFFFu;       // empty row slot (block rows < 65535)
 constexpr uint32_t kHeaderHi = 0xFFFF0000u; // header word: kHeaderHi | block_row
@@ -189,11 +192,17 @@ struct Chunk {
 // G rows are swizzled ((j + gi) mod NF) so every 8-lane phase of an LDS.128
 // touches 8 distinct bank quads (conflict-free for LPR >= 2 when NF % 4 == 0,
 // for LPR >= 4 when NF == 2).
+// Image of virtual column n < N (a 32-bit divide when the column count allows:
+// ~10x fewer instructions than the 64-bit one).
+__device__ __forceinline__ long long image_of(long long n, const KernelArgs& a) {
+    return a.N <= 0xFFFFFFFFLL ? static_cast<long long>(static_cast<uint32_t>(n) / static_cast<uint32_t>(a.S))
+                               : n / a.S;
+}
 // Output offset of virtual column n (-1 when n >= N): image b, pixel s ->
 // b*M*S + s; row r adds r*S.
 __device__ __forceinline__ long long col_offset(long long n, const KernelArgs& a) {
     if (n >= a.N) return -1;
-    const long long b = n / a.S;
+    const long long b = image_of(n, a);
     return b * static_cast<long long>(a.M_out) * a.S + (n - b * a.S);
 }
 
@@ -250,6 +259,7 @@ struct Exec {
 
     __device__ __forceinline__ void finish(const KernelArgs& a) {
         if (brow == kNoRow) return;
+        const bool relu = a.act_kind == 1 && a.hi == __int_as_float(0x7f800000);  // clamp(lo, +inf)
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
             const int col = static_cast<int>(lane_off[j] >> 2);  // first column of the quad
@@ -259,10 +269,17 @@ struct Exec {
                 if (r >= a.M_out) continue;  // padded row: computed, never stored (netdef.cpp:496-505)
                 const long long roff = static_cast<long long>(r) * a.S;
                 float4 v = acc[i][j];
-                v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
-                v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
-                v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
-                v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+                if (relu) {
+                    v.x = clamp_lo(v.x, a.lo);
+                    v.y = clamp_lo(v.y, a.lo);
+                    v.z = clamp_lo(v.z, a.lo);
+                    v.w = clamp_lo(v.w, a.lo);
+                } else {
+                    v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
+                    v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
+                    v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
+                    v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+                }
                 if constexpr (VEC) {
                     const long long o = ocol[j];
                     if (o >= 0) {
@@ -438,45 +455,64 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
     // image stride: K, or the whole matrix's K for a channel pass
     const long long KS = static_cast<long long>(ACC ? a.K_img : a.K) * a.S;
     for (int c = tid; c < T; c += nthreads) s_col[c] = col_offset(n0 + c, a);
+    // (running pointers and the column test outside the loops: ~5 instructions
+    // per copy instead of ~18, and the copies issue back to back)
     if constexpr (VEC) {
         constexpr int Q = T / 4;              // float4 per tile row (divides nthreads)
         const long long n = n0 + 4 * (tid % Q);
-        const bool valid = n < a.N;           // S % 4 == 0: a quad never straddles images
-        long long src = 0;
-        if (valid) {
-            const long long b = n / a.S;
-            src = b * KS + (n - b * a.S);
-        }
-        for (int k = tid / Q; k < a.K; k += nthreads / Q) {
-            float* dst = s_act + static_cast<size_t>(k) * T + 4 * (tid % Q);
-            if (valid)
-                cp_async16(dst, a.act + src + static_cast<long long>(k) * a.S);
-            else
+        const int k0 = tid / Q, kstep = nthreads / Q;
+        float* dst = s_act + static_cast<size_t>(k0) * T + 4 * (tid % Q);
+        const int dstep = kstep * T;
+        if (n < a.N) {                        // S % 4 == 0: a quad never straddles images
+            const long long b = image_of(n, a);
+            const float* src = a.act + (b * KS + (n - b * a.S)) + static_cast<long long>(k0) * a.S;
+            const long long sstep = static_cast<long long>(kstep) * a.S;
+#pragma unroll 2
+            for (int k = k0; k < a.K; k += kstep) {
+                cp_async16(dst, src);
+                dst += dstep;
+                src += sstep;
+            }
+        } else {
+            for (int k = k0; k < a.K; k += kstep) {
                 *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+                dst += dstep;
+            }
         }
     } else {
         const int c = tid % T;                // T divides nthreads (T <= 128)
         const long long n = n0 + c;
-        const bool valid = n < a.N;
-        long long src = 0;
-        if (valid) {
-            const long long b = n / a.S;
-            src = b * KS + (n - b * a.S);
-        }
-        for (int k = tid / T; k < a.K; k += nthreads / T) {
-            float* dst = s_act + static_cast<size_t>(k) * T + c;
-            if (valid)
-                cp_async4(dst, a.act + src + static_cast<long long>(k) * a.S);
-            else
+        const int k0 = tid / T, kstep = nthreads / T;
+        float* dst = s_act + static_cast<size_t>(k0) * T + c;
+        const int dstep = kstep * T;
+        if (n < a.N) {
+            const long long b = image_of(n, a);
+            const float* src = a.act + (b * KS + (n - b * a.S)) + static_cast<long long>(k0) * a.S;
+            const long long sstep = static_cast<long long>(kstep) * a.S;
+#pragma unroll 2
+            for (int k = k0; k < a.K; k += kstep) {
+                cp_async4(dst, src);
+                dst += dstep;
+                src += sstep;
+            }
+        } else {
+            for (int k = k0; k < a.K; k += kstep) {
                 *dst = 0.f;
+                dst += dstep;
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+// CAP: compiled for three 8-warp CTAs per SM (at most 80 registers). ptxas
+// otherwise settles on 83 for the unstructured 2-step kernels, which drops
+// the K <= 512 layers to two CTAs per SM (measured: MBv1 pw5 237.6 vs 215.2 us,
+// pw7 215.1 vs 206.8 us); the 16-warp launches of wide tiles use CAP = false.
+constexpr int kCapThreads = 256, kCapBlocks = 3;
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false>
+__global__ void __launch_bounds__(CAP ? kCapThreads : kThreads, CAP ? kCapBlocks : kMinBlocks)
 spmm_bcsr_kernel(const KernelArgs a) {
     using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
     constexpr int G = E::G;
