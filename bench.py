@@ -503,13 +503,20 @@ def time_steps(sp, dev_layers, steps, warmup, stream, dist, dev, flush_buf, per_
 
     cdev = torch.device("cuda", dev)
 
+    # each layer's call bound once to its (fixed) device buffers: one C-ABI call
+    # per launch without the per-call torch attribute reads, which otherwise
+    # bound the batch-1 configs (13 launches of ~5-8 us each) on the host
+    calls = [sp.bind_batched(dw, a, b, fused, o, cfgk, stream=stream) for dw, a, b, o, fused, cfgk in dev_layers]
+
     def step(evs=None):
-        for li, (dw, a, b, o, fused, cfgk) in enumerate(dev_layers):
-            if evs is not None:
-                evs[li][0].record(stream)
-            sp.spmm_batched_into(dw, a, b, fused, o, cfgk, stream=stream)
-            if evs is not None:
-                evs[li][1].record(stream)
+        if evs is None:
+            for call in calls:
+                call()
+            return
+        for li, call in enumerate(calls):
+            evs[li][0].record(stream)
+            call()
+            evs[li][1].record(stream)
 
     def flush():
         if flush_buf is not None:

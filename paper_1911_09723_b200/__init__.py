@@ -48,7 +48,7 @@ from .bcsr import (
 _DEVICE = {
     "DeviceBcsr": "spmm", "DeviceModel": "spmm", "parse_model_status": "spmm",
     "dense_gemm_batched_into": "spmm", "spconv_1x1": "spmm", "spmm": "spmm",
-    "spmm_batched_into": "spmm", "spmm_host_batched": "spmm", "spmm_into": "spmm",
+    "spmm_batched_into": "spmm", "bind_batched": "spmm", "spmm_host_batched": "spmm", "spmm_into": "spmm",
     "spmm_layer": "spmm", "LIB_PATH": "_capi", "launch_count": "_capi", "cache_stats": "_capi",
 }
 

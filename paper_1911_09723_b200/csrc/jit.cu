@@ -317,8 +317,6 @@ std::string gen_source(int M, int K, int BH, const uint32_t* row_ptr, const uint
          " const float* __restrict__ bias, long long N, long long S, float lo, float hi,"
          " const float* __restrict__ res, u64 one) {\n"
       << "  extern __shared__ float4 smem4[];\n"
-      << "  asm volatile(\"griddepcontrol.launch_dependents;\\n\" ::: \"memory\");\n"
-      << "  asm volatile(\"griddepcontrol.wait;\\n\" ::: \"memory\");  // after the previous kernel (PDL)\n"
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  float* ring = reinterpret_cast<float*>(smem4) + warp * (P * KC * " << 32 * key.cpl << ");\n"
       << "  const int seg = seg_of[blockIdx.x], rank = rank_of[blockIdx.x];\n"
@@ -357,8 +355,6 @@ std::string gen_direct(int M, int K, int BH, const uint32_t* row_ptr, const uint
          " float* __restrict__ out, const float* __restrict__ bias, long long N, long long S,"
          " float lo, float hi, const float* __restrict__ res, unsigned long long one,"
          " const float* __restrict__ dwin, int H, int W, int OW, int pt, int pl, float dlo, float dhi) {\n"
-      << "  asm volatile(\"griddepcontrol.launch_dependents;\\n\" ::: \"memory\");\n"
-      << "  asm volatile(\"griddepcontrol.wait;\\n\" ::: \"memory\");  // after the previous kernel (PDL)\n"
       << "  const long long n = blockIdx.x * 128LL + threadIdx.x;\n"
       << "  if (n >= N) return;\n"
       << "  const long long b = n / S, s = n - b * S;\n"
@@ -667,7 +663,7 @@ void jit_release(spcv_cu_weights* w) {
     w->jit.clear();
 }
 
-int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st, const JitDwArgs* dw, bool pdl) {
+int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st, const JitDwArgs* dw) {
     long long N = a.N, S = a.S;
     float lo = a.lo, hi = a.hi;
     const float* act = a.act;
@@ -678,15 +674,8 @@ int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st,
     JitDwArgs d = dw ? *dw : JitDwArgs{};
     void* args[] = {&act, &out, &bias, &N, &S, &lo, &hi, &res, &one,
                     &d.in, &d.H, &d.W, &d.OW, &d.pad_t, &d.pad_l, &d.lo, &d.hi};
-    // programmatic dependent launch: the generated kernels wait (griddepcontrol.wait)
-    // before touching memory the previous kernel on the stream may produce
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.stream = st;
-    cfg.attrs = pdl ? attr : nullptr;
-    cfg.numAttrs = pdl ? 1 : 0;
     if (v->direct) {
         const long long blocks = (N + 127) / 128;
         if (blocks > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "jit: grid too large");

@@ -55,7 +55,7 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     spcvk::KernelArgs at = a;
     at.tail_start = g.tail_start;
     at.tail_split = g.tail_split;
-    SPCV_CUDA(launch_kernel(kern, grid, dim3(g.nwarps * 32), g.smem, st, a.pdl, at));
+    SPCV_CUDA(launch_kernel(kern, grid, dim3(g.nwarps * 32), g.smem, st, at));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }

@@ -54,10 +54,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
 spmm_small_kernel(const SmallArgs a) {
     const int lane = threadIdx.x & 31;
     const int br = blockIdx.y * kSmallWarps + (threadIdx.x >> 5);
-    if (br >= a.brows) {
-        pdl_trigger();
-        return;
-    }
+    if (br >= a.brows) return;
     const long long n = static_cast<long long>(blockIdx.x) * 32 + lane;
     const bool valid = n < a.N;
     long long abase = 0, obase = 0;
@@ -68,17 +65,23 @@ spmm_small_kernel(const SmallArgs a) {
         obase = img * a.M_out * a.S + s;
     }
     const float* act = a.act + abase;
-    pdl_trigger();
-    // The row's first 32 blocks come from the head table (no dependency on
-    // row_ptr, loaded in the same round trip); later groups of 32 from
-    // col_idx / values at row_ptr[br] + 32.
-    const size_t h = static_cast<size_t>(br) * 32 + lane;
-    uint32_t kcol = __ldg(a.head_col + h);
-    float wv[BH];
-#pragma unroll
-    for (int i = 0; i < BH; ++i) wv[i] = __ldg(a.head_val + h * BH + i);
+    // The row's first 32 blocks come from the head table when the matrix has
+    // one (no dependency on row_ptr, loaded in the same round trip), else from
+    // col_idx / values at row_ptr[br]; later groups of 32 from there too.
     const uint32_t rb = __ldg(a.row_ptr + br), re = __ldg(a.row_ptr + br + 1);
-    pdl_wait();  // activations, bias and residual may come from the previous kernel on the stream
+    uint32_t kcol;
+    float wv[BH];
+    if (a.head_col != nullptr) {
+        const size_t h = static_cast<size_t>(br) * 32 + lane;
+        kcol = __ldg(a.head_col + h);
+#pragma unroll
+        for (int i = 0; i < BH; ++i) wv[i] = __ldg(a.head_val + h * BH + i);
+    } else {
+        const bool mine = rb + lane < re;
+        kcol = mine ? __ldg(a.col_idx + rb + lane) : 0u;
+#pragma unroll
+        for (int i = 0; i < BH; ++i) wv[i] = mine ? __ldg(a.values + static_cast<size_t>(rb + lane) * BH + i) : 0.0f;
+    }
     float acc[BH];
 #pragma unroll
     for (int i = 0; i < BH; ++i) {
@@ -129,19 +132,19 @@ spmm_small_kernel(const SmallArgs a) {
 namespace spcv_detail {
 
 template <int BH>
-static int launch_small_bh(const spcvk::SmallArgs& a, bool strict, bool pdl, cudaStream_t st) {
+static int launch_small_bh(const spcvk::SmallArgs& a, bool strict, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((a.N + 31) / 32),
                     static_cast<unsigned>((a.brows + spcvk::kSmallWarps - 1) / spcvk::kSmallWarps));
     const dim3 threads(spcvk::kSmallWarps * 32);
     auto kern = strict ? (a.residual ? spcvk::spmm_small_kernel<BH, true, true> : spcvk::spmm_small_kernel<BH, true, false>)
                        : (a.residual ? spcvk::spmm_small_kernel<BH, false, true> : spcvk::spmm_small_kernel<BH, false, false>);
-    SPCV_CUDA(launch_kernel(kern, grid, threads, 0, st, pdl, a));
+    SPCV_CUDA(launch_kernel(kern, grid, threads, 0, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SPCV_OK;
 }
 
 int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& k, bool strict, cudaStream_t st) {
-    if (!w->d_row_ptr || !w->d_col_idx || !w->d_head_col) return SPCV_ERR_UNSUPPORTED;
+    if (!w->d_row_ptr || !w->d_col_idx) return SPCV_ERR_UNSUPPORTED;
     if ((k.N + 31) / 32 > 0x7FFFFFFFLL || w->brows > 65535 * spcvk::kSmallWarps) return SPCV_ERR_UNSUPPORTED;
     spcvk::SmallArgs a;
     a.act = k.act;
@@ -162,9 +165,9 @@ int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& k, bool stri
     a.lo = k.lo;
     a.hi = k.hi;
     switch (w->block_h) {
-        case 1: return launch_small_bh<1>(a, strict, k.pdl, st);
-        case 2: return launch_small_bh<2>(a, strict, k.pdl, st);
-        default: return launch_small_bh<4>(a, strict, k.pdl, st);
+        case 1: return launch_small_bh<1>(a, strict, st);
+        case 2: return launch_small_bh<2>(a, strict, st);
+        default: return launch_small_bh<4>(a, strict, st);
     }
 }
 

@@ -67,8 +67,8 @@ Knobs Knobs::from_env() {
     k.jit_interleave = static_cast<int>(get("SPCV_JIT_INTERLEAVE", 1));
     k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
     k.small = static_cast<int>(get("SPCV_SMALL", 1));
-    k.pdl = static_cast<int>(get("SPCV_PDL", 1));
     k.regcap = get("SPCV_REGCAP", 1) != 0;
+    k.small_head = get("SPCV_SMALL_HEAD", 1) != 0;
     return k;
 }
 
@@ -478,17 +478,18 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
         }
     }
     // head table of the few-column kernel: each block row's first 32 blocks
-    std::vector<uint32_t> head_col(static_cast<size_t>(brows) * 32, ~0u);
-    std::vector<float> head_val(static_cast<size_t>(brows) * 32 * BH, 0.0f);
-    for (int r = 0; r < brows; ++r)
+    const size_t head_rows = kn.small_head ? static_cast<size_t>(brows) : 0;
+    std::vector<uint32_t> head_col(head_rows * 32, ~0u);
+    std::vector<float> head_val(head_rows * 32 * BH, 0.0f);
+    for (int r = 0; r < static_cast<int>(head_rows); ++r)
         for (uint32_t b = row_ptr[r], i = 0; b < row_ptr[r + 1] && i < 32; ++b, ++i) {
             head_col[static_cast<size_t>(r) * 32 + i] = col_idx[b];
             for (int j = 0; j < BH; ++j)
                 head_val[(static_cast<size_t>(r) * 32 + i) * BH + j] = values[static_cast<size_t>(b) * BH + j];
         }
     int rc = SPCV_OK;
-    if ((rc = upload(&w->d_head_col, head_col.data(), head_col.size())) ||
-        (rc = upload(&w->d_head_val, head_val.data(), head_val.size())) ||
+    if ((head_rows && ((rc = upload(&w->d_head_col, head_col.data(), head_col.size())) ||
+                       (rc = upload(&w->d_head_val, head_val.data(), head_val.size())))) ||
         (rc = upload(&w->d_nnz, nnz.data(), nnz.size())) ||
         (rc = upload(&w->d_delta, delta.data(), delta.size())) ||
         (rc = upload(&w->d_values, values, nvalues)) ||
@@ -814,8 +815,6 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.tail_split = 1;
     a.tail_pref = -1;
     a.split_pref = 0;
-    a.pdl = w->knobs.pdl > 1 ||
-            (w->knobs.pdl == 1 && static_cast<double>(w->nblocks) * w->block_h * N <= kPdlMaxProducts);
     a.one2 = 0x3f8000003f800000ULL;
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
@@ -831,7 +830,7 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
                                  reinterpret_cast<uintptr_t>(act), reinterpret_cast<uintptr_t>(out), a.M_out, &jv);
     if (kind == SPCV_KERNEL_JIT) {
         // A failed compile (recorded, never retried) falls back to the other kernels.
-        if (const JitVariant* v = jit_build(w, jv)) return jit_launch(v, a, st, nullptr, a.pdl);
+        if (const JitVariant* v = jit_build(w, jv)) return jit_launch(v, a, st);
     }
     if (kind == SPCV_KERNEL_SMALL) {
         const int rc = launch_small(w, a, strict, st);

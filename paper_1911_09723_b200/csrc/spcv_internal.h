@@ -34,7 +34,7 @@ struct Knobs {
     int jit_direct_maxk = 0, jit_interleave = 1;       // SPCV_JIT_DIRECT_MAXK / SPCV_JIT_INTERLEAVE
     int pass_k = 0;        // SPCV_PASS_K: run matrices wider than this as channel passes of this width
     int small = 1;         // SPCV_SMALL: 0 = never the few-column kernel, 2 = always (single pass)
-    int pdl = 1;           // SPCV_PDL: programmatic dependent launch 0 = never, 1 = short calls, 2 = always
+    bool small_head = true;  // SPCV_SMALL_HEAD=0: no per-row head table for the few-column kernel
     int regcap = 1;        // SPCV_REGCAP=0: never the 80-register build of the unstructured 2-step kernels
     static Knobs from_env();
     long long geometry_key() const {
@@ -153,10 +153,6 @@ int launch_bh4(const spcvk::KernelArgs&, const spcv_cu_weights*, long long ntile
 // straight from global memory. SPCV_ERR_UNSUPPORTED when it cannot serve.
 int launch_small(const spcv_cu_weights* w, const spcvk::KernelArgs& a, bool strict, cudaStream_t st);
 constexpr double kSmallMaxProducts = 8.0e6;  // products (stored values x columns) per call
-// Programmatic dependent launch for calls of at most this many products
-// (measured: MBv1 at 32 images per GPU 0.433 -> 0.428 ms per step; at 256
-// images, ~15x the work per launch, it cost 0.3 %)
-constexpr double kPdlMaxProducts = 2.7e8;
 
 // Weight-specialised kernels (jit.cu): one persistent CTA of kJitWarps warps
 // per SM, a kJitStages-deep ring of [32 channels][64 columns] fp32 per warp.
@@ -177,7 +173,7 @@ inline const JitVariant* jit_prepare(const spcv_cu_weights* w, const JitKey& key
     return jit_build(w, jit_plan(w, key));
 }
 int jit_launch(const JitVariant* v, const spcvk::KernelArgs& a, cudaStream_t st,
-               const JitDwArgs* dw = nullptr, bool pdl = false);
+               const JitDwArgs* dw = nullptr);
 // Depthwise 3x3 (host copies of its weights/bias) fused into the next sparse
 // 1x1 layer through the direct JIT variant; SPCV_ERR_UNSUPPORTED when that
 // variant does not serve the matrix (the caller then runs the two layers).
@@ -189,21 +185,17 @@ void jit_release(spcv_cu_weights* w);
 
 }  // namespace spcv_detail
 
-// Launch `kern` on `st`, with programmatic stream serialization when `pdl`
-// (the kernel then overlaps its prologue with the previous kernel's tail and
-// waits in pdl_wait before touching data that kernel may produce).
+// Launch `kern` on `st`. (Programmatic dependent launch was measured and
+// removed: griddepcontrol in the kernels costs ~1 us per batch-1 launch even
+// without the launch attribute, and with it the 32-image MBv1 step was 3.7 %
+// slower — profiles/r2_notes.md, r2g.)
 template <typename Kern, typename... Args>
-cudaError_t launch_kernel(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+cudaError_t launch_kernel(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cfg.attrs = pdl ? attr : nullptr;
-    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

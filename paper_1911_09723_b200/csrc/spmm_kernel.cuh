@@ -66,7 +66,6 @@ struct KernelArgs {
     int steps;               // steps per chunk of `stream` (host-side dispatch)
     int tail_pref;           // host-side: tail split chosen by the autotuner (-1: heuristic, 0: none)
     int split_pref;          // host-side: CTAs per tile chosen by the autotuner (0: heuristic)
-    bool pdl;                // host-side: launch with programmatic stream serialization
     // {1.0f, 1.0f} as f32x2, passed at run time so ptxas cannot fold the
     // strict pair mul.rn.f32x2 + fma.rn.f32x2(acc, one, p) into one FFMA2.
     unsigned long long one2;
@@ -86,14 +85,6 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
-
-// Programmatic dependent launch (the launch sets the programmatic stream
-// serialization attribute): pdl_wait blocks until the previous kernel on the
-// stream has completed and its writes are visible — every read of data it may
-// produce and every global write happen after it; pdl_trigger lets the next
-// kernel start launching. Both are no-ops without the attribute.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 __device__ __forceinline__ uint2 ldg_stream2(const void* p) {
     uint2 v;
@@ -537,7 +528,6 @@ spmm_bcsr_kernel(const KernelArgs a) {
     }
     const long long n0 = tile * T;
 
-    pdl_trigger();  // the next launch on the stream may start its prologue once all our CTAs are resident
     for (int i = tid; i < T / 4; i += nthreads)  // zero row: target of padded steps
         reinterpret_cast<float4*>(s_act + static_cast<size_t>(a.K) * T)[i] =
             make_float4(0.f, 0.f, 0.f, 0.f);
@@ -549,7 +539,6 @@ spmm_bcsr_kernel(const KernelArgs a) {
     // ---- this warp's contiguous slice of the weight stream ----
     // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
     // consecutive schedule bins (balanced by the packer's LPT at every split).
-    // (weights are written only when packed: safe to read before pdl_wait)
     const int per = kBins / ((nthreads >> 5) * nparts);
     const int bin0 = (part * (nthreads >> 5) + warp) * per;
     uint32_t pos = __ldg(a.bin_beg + bin0);
@@ -560,8 +549,7 @@ spmm_bcsr_kernel(const KernelArgs a) {
     for (int d = 0; d < kRing; ++d)
         ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + d, end, gi);
 
-    // ---- after the previous kernel on the stream: bias, column offsets and the [K][T] tile ----
-    pdl_wait();
+    // ---- bias, column offsets and the [K][T] tile ----
     if (a.bias != nullptr) {  // logical rows from bias; padded rows (never stored) get 0
         for (int i = tid; i < a.M_out; i += nthreads) cp_async4(s_bias + i, a.bias + i);
         for (int i = a.M_out + tid; i < a.M; i += nthreads) s_bias[i] = 0.0f;

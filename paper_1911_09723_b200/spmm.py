@@ -248,6 +248,52 @@ def spmm_batched_into(w: DeviceBcsr, act, bias, fused: Activation, out,
         cfg.m, cfg.n, _mode(cfg), sptr))
 
 
+def bind_batched(w: DeviceBcsr, act, bias, fused: Activation, out,
+                 cfg: MicrokernelConfig | None = None, stream=None):
+    """spmm_batched_into with its arguments checked and converted once: returns
+    a zero-argument callable that launches the same call again (serving loops
+    over fixed buffers; the tensors must stay alive and keep their addresses).
+    Each invocation is one C-ABI call (spcv_cu_spmm_into, its checks included)
+    without the per-call torch attribute reads, ~2 us instead of ~10 us of host
+    time — what bounds a batch-1 layer chain launched from Python."""
+    import torch
+
+    cfg = cfg or MicrokernelConfig(n=w.block_h)
+    if act.dim() == 3:
+        act = act.unsqueeze(0)
+        out = out.unsqueeze(0)
+    if act.device.type != "cuda" or out.device.type != "cuda":
+        raise DeviceError("bind_batched: tensors must be on a CUDA device")
+    if act.dtype != torch.float32 or out.dtype != torch.float32:
+        raise ShapeError("bind_batched: float32 tensors required")
+    if not (act.is_contiguous() and out.is_contiguous()):
+        raise LayoutError("bind_batched: contiguous NCHW tensors required")
+    B, K, H, W = act.shape
+    if out.shape[0] != B:
+        raise ShapeError("bind_batched: batch mismatch")
+    bptr, blen = None, 0
+    if bias is not None:
+        if bias.device.type != "cuda" or bias.dtype != torch.float32:
+            raise ShapeError("bind_batched: bias must be a CUDA float32 tensor")
+        bptr, blen = bias.data_ptr(), bias.numel()
+    if stream is None:
+        stream = torch.cuda.current_stream(act.device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    fn = lib.spcv_cu_spmm_into
+    args = [w.handle, act.data_ptr(), _capi.LAYOUT_CHW, B, K, H, W, bptr, blen, fused.kind, fused.lo,
+            fused.hi, out.data_ptr(), _capi.LAYOUT_CHW, out.shape[1], out.shape[2], out.shape[3],
+            cfg.m, cfg.n, _mode(cfg), sptr]
+    cargs = tuple(a if a is None or isinstance(a, ctypes._SimpleCData) else t(a) for t, a in zip(fn.argtypes, args))
+    keep = (w, act, bias, out, stream)  # the bound buffers live as long as the callable
+
+    def call(_fn=fn, _a=cargs, _keep=keep):
+        rc = _fn(*_a)
+        if rc:
+            _raise(rc)
+
+    return call
+
+
 def dense_gemm_batched_into(w, act, bias, fused: Activation, out, cfg: MicrokernelConfig | None = None,
                             stream=None) -> None:
     """Dense fp32 baseline (reference dense_gemm_into, kernels.cpp:345-373) on

@@ -866,6 +866,34 @@ def test_randomized_shapes_bit_exact(oracle, monkeypatch, kernel):
         assert np.array_equal(bits(got), bits(want)), (case, K, M, bh, H, W, B, sparsity)
 
 
+def test_bound_call_equals_direct_call(oracle):
+    """bind_batched: arguments checked and converted once, every invocation one
+    C-ABI call — same bits as spmm_batched_into, one counted launch each, and
+    the C-ABI's own argument checks still run at call time."""
+    import torch
+
+    layer = CONFIGS["c1"]["layers"]()[0]
+    d = make_layer_data(layer, 2, 77)
+    dw = sp.DeviceBcsr(d.weights)
+    a = torch.from_numpy(d.act).cuda()
+    b = torch.from_numpy(d.bias).cuda()
+    o = torch.full((2, layer.cout, layer.h, layer.w), float("nan"), device="cuda")
+    call = sp.bind_batched(dw, a, b, act_of(layer.act), o)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act).reshape(o.shape)
+    for _ in range(3):
+        o.fill_(float("nan"))
+        n0 = sp.launch_count()
+        call()
+        torch.cuda.synchronize()
+        assert sp.launch_count() == n0 + 1
+        assert np.array_equal(bits(o.cpu().numpy()), bits(want))
+    bad = sp.bind_batched(dw, a, b[:-1].contiguous(), act_of(layer.act), o)  # bias one short
+    with pytest.raises(sp.ShapeError):
+        bad()
+    with pytest.raises(sp.DeviceError):
+        sp.bind_batched(dw, a.cpu(), b, act_of(layer.act), o)
+
+
 # ------------------------------------ launch geometry: tail and row splits
 @pytest.mark.parametrize("env", [{"SPCV_TAIL": "0"}, {"SPCV_TAIL": "2"}, {"SPCV_TAIL": "4"}, {"SPCV_TAIL": "8"},
                                  {"SPCV_SPLIT": "2", "SPCV_TAIL": "4"}, {"SPCV_NWARPS": "8", "SPCV_TAIL": "8"},
@@ -978,17 +1006,14 @@ def test_default_kernel_choice_by_column_count(monkeypatch):
     assert sp.DeviceBcsr(d13.weights).kernel_for(256, 7, 7) == "tile"
 
 
-@pytest.mark.parametrize("pdl", ["2", "0"])
-def test_chained_layers_on_one_stream_bit_exact(oracle, monkeypatch, pdl):
+def test_chained_layers_on_one_stream_bit_exact(oracle):
     """Layers launched back to back on one stream, each consuming the previous
     layer's output and overwriting a buffer an earlier layer read, across the
-    three kernels (weight-specialised, tile, few-column): with programmatic
-    dependent launch (SPCV_PDL=2: always; the default uses it for short calls) every kernel waits for its
-    predecessor before reading its input or writing its output, so the chain
-    equals the oracle applied layer by layer, bit for bit."""
+    three kernels (weight-specialised, tile, few-column): stream order alone
+    makes every kernel see its predecessor's output, so the chain equals the
+    oracle applied layer by layer, bit for bit."""
     import torch
 
-    monkeypatch.setenv("SPCV_PDL", pdl)
     rng = np.random.default_rng(77)
     chans = [48, 64, 96, 96, 128, 64, 32]  # K=48 (JIT direct), larger K (tile / few-column)
     H = W = 14
