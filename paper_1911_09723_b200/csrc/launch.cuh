@@ -25,12 +25,13 @@ struct Geometry {
 
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref,
-                  int max_threads);
+                  int max_threads, size_t scratch_per_warp);
 
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false,
+          bool COAL = false>
 int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long ntiles, int sms,
                  cudaStream_t st) {
-    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC, CAP>;
+    auto kern = spcvk::spmm_bcsr_kernel<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC, CAP, COAL>;
     // cudaFuncSetAttribute is per device; remember which devices are done.
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -48,7 +49,8 @@ int launch_one_r(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long
     const long long k[7] = {ntiles, dev, w->cols, w->rows, w->T, w->knobs.geometry_key(),
                             a.tail_pref * 64LL + a.split_pref};
     if (!std::equal(k, k + 7, key)) {
-        g = geometry(kern, w, ntiles, sms, a.tail_pref, a.split_pref, CAP ? spcvk::kCapThreads : spcvk::kThreads);
+        g = geometry(kern, w, ntiles, sms, a.tail_pref, a.split_pref, CAP ? spcvk::kCapThreads : spcvk::kThreads,
+                     COAL ? sizeof(float) * spcvk::coal_scratch_floats(32 / LPR, LPR * NF * 4) : 0);
         std::copy(k, k + 7, key);
     }
     dim3 grid(static_cast<unsigned>(g.grid_x), static_cast<unsigned>(g.split));
@@ -82,6 +84,15 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
             3 * smem_bytes(w->cols, w->rows, w->T) <= kSmemLimit)
             return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true, false, true>(a, w, ntiles, sms, st)
                               : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false, false, true>(a, w, ntiles, sms, st);
+    }
+    // Unaligned layouts: the build whose epilogue stores row by row through a
+    // per-warp scratch, where the call's first launches measured it faster
+    // (spcv_cu.cu: tuned_geometry) or SPCV_COAL=2 forces it.
+    if constexpr (!VEC) {
+        if (a.coal)
+            return a.residual
+                       ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true, false, false, true>(a, w, ntiles, sms, st)
+                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false, false, false, true>(a, w, ntiles, sms, st);
     }
     return a.residual ? launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, true>(a, w, ntiles, sms, st)
                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
@@ -131,10 +142,13 @@ int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt
 // split tiles across CTAs (row split) until the grid covers the GPU.
 template <typename Kern>
 Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms, int tail_pref, int split_pref,
-                  int max_threads) {
+                  int max_threads, size_t scratch_per_warp) {
     Geometry g;
     g.ntiles = ntiles;
-    g.smem = smem_bytes(w->cols, w->rows, w->T);
+    // (the per-warp output scratch of the coalesced epilogue sits after the bias, 16 B-aligned)
+    const size_t base = scratch_per_warp ? smem_bytes(w->cols, (w->rows + 3) & ~3, w->T)
+                                         : smem_bytes(w->cols, w->rows, w->T);
+    g.smem = base + 16 * scratch_per_warp;
     int best = 0, per_sm = 1;
     g.nwarps = std::min(16, max_threads / 32);
     const Knobs& kn = w->knobs;
@@ -142,12 +156,15 @@ Geometry geometry(Kern kern, const spcv_cu_weights* w, long long ntiles, int sms
         if (nw * 32 > max_threads) continue;
         if (kn.nwarps && kn.nwarps != nw) continue;
         int ctas = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, g.smem) != cudaSuccess)
+        const size_t smem_nw = base + nw * scratch_per_warp;
+        if (smem_nw > kSmemLimit ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, nw * 32, smem_nw) != cudaSuccess)
             ctas = 0;
         if (ctas * nw > best) {
             best = ctas * nw;
             per_sm = ctas;
             g.nwarps = nw;
+            g.smem = smem_nw;
         }
     }
     g.split = 1;

@@ -14,7 +14,6 @@
 #include <cstring>
 #include <mutex>
 #include <new>
-#include <queue>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -68,6 +67,7 @@ Knobs Knobs::from_env() {
     k.pass_k = static_cast<int>(get("SPCV_PASS_K", 0));
     k.small = static_cast<int>(get("SPCV_SMALL", 1));
     k.regcap = get("SPCV_REGCAP", 1) != 0;
+    k.coal = static_cast<int>(get("SPCV_COAL", 1)) & 3;
     k.small_head = get("SPCV_SMALL_HEAD", 1) != 0;
     return k;
 }
@@ -134,8 +134,6 @@ Layout choose_layout(int K, int M, int block_h, const Knobs& kn) {
         }
     return {0, NF, 0};
 }
-
-int bitrev3(int i) { return ((i & 1) << 2) | (i & 2) | ((i & 4) >> 2); }
 
 struct DevProps {
     int sms = 148;
@@ -347,9 +345,8 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
     }
 
     // Row bucketing: sort block rows by nnz (descending), form groups of G
-    // neighbours (similar lengths -> little predication), then LPT the groups
-    // over kBins bins. Bin b = warp*kMaxSplit + i; ties go to the bin whose
-    // (bit-reversed i, warp) is smallest so every split level stays balanced.
+    // neighbours (similar lengths -> little predication), then balance the
+    // groups over kBins bins at every power-of-two level (see build below).
     std::vector<int> order(brows);
     for (int r = 0; r < brows; ++r) order[r] = r;
     std::stable_sort(order.begin(), order.end(),
@@ -363,6 +360,7 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
         size_t nchunks = 0;
     };
     auto build = [&](int STEPS, Built& out) {
+        const int group_overhead = STEPS == 2 ? 3 : 2;  // a header + epilogue pass costs about this many chunks
         std::vector<int> gchunks(ngroups);
         for (int g = 0; g < ngroups; ++g) {
             uint32_t mx = 0;
@@ -372,22 +370,30 @@ int pack_impl(int rows, int cols, int block_h, const uint32_t* row_ptr, size_t r
             }
             gchunks[g] = static_cast<int>((mx + STEPS - 1) / STEPS);
         }
+        // Longest group first, each one walked down the binary tree over the
+        // kBins bins into the lighter half at every level: any aligned range
+        // of kBins / V bins is the work of one of V virtual warps (warps per
+        // CTA x CTAs sharing a tile), so every V the launcher may pick gets
+        // balanced loads. (A flat LPT over the bins balances nothing while
+        // there are fewer groups than bins: the longest group of every round
+        // of 16 landed on warp 0 — measured on the per-CTA timeline, the
+        // slowest warp finished 9-33 % after the first: pw13 +4.0 of 46 us,
+        // c5 @90 % +23 of 71 us.)
         std::vector<std::vector<int>> bins(kBins);
-        using Item = std::tuple<long long, int, int>;  // load, priority, bin
-        std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
-        for (int b = 0; b < kBins; ++b) {
-            const int warp = b / kMaxSplit, i = b % kMaxSplit;
-            heap.emplace(0LL, bitrev3(i) * kWarps + warp, b);
-        }
+        std::vector<long long> load(2 * kBins, 0);  // heap-ordered tree: node 1 = all bins, leaves kBins..2*kBins-1
         std::vector<int> gorder(ngroups);
         for (int g = 0; g < ngroups; ++g) gorder[g] = g;
         std::stable_sort(gorder.begin(), gorder.end(),
                          [&](int a, int b) { return gchunks[a] > gchunks[b]; });
         for (int g : gorder) {
-            auto [load, prio, b] = heap.top();
-            heap.pop();
-            bins[b].push_back(g);
-            heap.emplace(load + gchunks[g] + 2, prio, b);  // +2: header + epilogue
+            const long long cost = gchunks[g] + group_overhead;  // header + epilogue, in chunks
+            int node = 1;
+            while (node < kBins) {
+                load[node] += cost;
+                node = 2 * node + (load[2 * node] <= load[2 * node + 1] ? 0 : 1);
+            }
+            load[node] += cost;
+            bins[node - kBins].push_back(g);
         }
 
         // Chunk (spmm_kernel.cuh, Fmt): index area G x STEPS u16 (padded to 16 B),
@@ -580,6 +586,12 @@ extern "C" int spcv_cu_weights_kernel(spcv_cu_weights* w, int mode, int* kernel)
     return SPCV_OK;
 }
 
+#ifdef SPCV_TIMELINE
+// Timeline builds only (tools/timeline.py): device buffer of 8 u64 per CTA of the next tile-kernel launches.
+static unsigned long long* g_timeline = nullptr;
+extern "C" void spcvx_set_timeline(unsigned long long* buf) { g_timeline = buf; }
+#endif
+
 // ------------------------------------------------------------------- launch
 namespace {
 int pick_kernel(const spcv_cu_weights* w, long long N, long long S, long long ntiles, int sms, bool vec, bool pass,
@@ -661,18 +673,21 @@ int check_args(const spcv_cu_weights* w, int act_layout, int images, int act_c, 
 struct TunedGeometry {
     int tail = -1;   // -1: heuristic
     int split = 0;   // 0: heuristic
+    int coal = 0;    // 1: the coalesced-epilogue build (unaligned layouts)
 };
 
 template <typename Run>
 TunedGeometry tuned_geometry(const spcv_cu_weights* w, const spcvk::KernelArgs& a, long long N, long long ntiles,
-                             int sms, bool strict, bool vec, cudaStream_t st, Run&& run) {
+                             int sms, bool strict, bool vec, bool coal_ok, cudaStream_t st, Run&& run) {
     TunedGeometry none;
+    none.coal = coal_ok && w->knobs.coal == 2;
     if (!w->knobs.autotune || w->knobs.tail >= 0) return none;
     const long long key = N * 8 + (strict ? 4 : 0) + (vec ? 2 : 0);
     {
         std::lock_guard<std::mutex> lk(w->tune_mu);
         for (const auto& kv : w->tuned_tail)
-            if (kv.first == key) return TunedGeometry{kv.second % 64 - 1, kv.second / 64};  // also inside a capture
+            if (kv.first == key)  // also inside a capture
+                return TunedGeometry{kv.second % 64 - 1, kv.second / 64 % 64, coal_ok ? kv.second / 4096 : 0};
     }
     if (a.acc_in) return none;  // a later channel pass reads out: not repeatable in place
     if (a.residual) {  // repeated launches are idempotent unless out overlaps the residual
@@ -688,9 +703,13 @@ TunedGeometry tuned_geometry(const spcv_cu_weights* w, const spcvk::KernelArgs& 
         if (e0) cudaEventDestroy(e0);
         return none;
     }
-    std::vector<TunedGeometry> cands = {{-1, 0}, {0, 0}, {2, 0}, {4, 0}};
+    std::vector<TunedGeometry> cands = {{-1, 0, none.coal}, {0, 0, none.coal}, {2, 0, none.coal}, {4, 0, none.coal}};
     if (ntiles < 2LL * sms && w->knobs.split == 0)  // few tiles: the row split too
-        for (int sp : {1, 2, 4, 8}) cands.push_back(TunedGeometry{-1, sp});
+        for (int sp : {1, 2, 4, 8}) cands.push_back(TunedGeometry{-1, sp, none.coal});
+    if (coal_ok && w->knobs.coal == 1) {  // unaligned layout: each geometry with the coalesced epilogue too
+        const size_t n = cands.size();
+        for (size_t i = 0; i < n; ++i) cands.push_back(TunedGeometry{cands[i].tail, cands[i].split, 1});
+    }
     TunedGeometry best;
     float best_ms = 0.0f;
     uint64_t runs = 0;  // tuning launches are not the caller's work: not counted
@@ -698,6 +717,7 @@ TunedGeometry tuned_geometry(const spcv_cu_weights* w, const spcvk::KernelArgs& 
         spcvk::KernelArgs t = a;
         t.tail_pref = cand.tail;
         t.split_pref = cand.split;
+        t.coal = cand.coal;
         if (run(t) != SPCV_OK) continue;  // warm-up (geometry, L2)
         ++runs;
         cudaEventRecord(e0, st);
@@ -714,7 +734,7 @@ TunedGeometry tuned_geometry(const spcv_cu_weights* w, const spcvk::KernelArgs& 
     cudaEventDestroy(e1);
     g_launches.fetch_sub(runs, std::memory_order_relaxed);
     std::lock_guard<std::mutex> lk(w->tune_mu);
-    w->tuned_tail.emplace_back(key, best.split * 64 + best.tail + 1);
+    w->tuned_tail.emplace_back(key, best.coal * 4096 + best.split * 64 + best.tail + 1);
     return best;
 }
 
@@ -816,6 +836,10 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
     a.tail_pref = -1;
     a.split_pref = 0;
     a.one2 = 0x3f8000003f800000ULL;
+    a.coal = 0;
+#ifdef SPCV_TIMELINE
+    a.tl = g_timeline;
+#endif
     const long long ntiles = (N + w->T - 1) / w->T;
     if (ntiles > 0x7FFFFFFFLL) return fail(SPCV_ERR_UNSUPPORTED, "spmm: too many column tiles");
     const int sms = props_for(dev).sms;
@@ -844,9 +868,16 @@ int launch(const spcv_cu_weights* w, const float* act, int images, int act_h, in
             default: return launch_bh4(args, w, ntiles, sms, strict, vec, st);
         }
     };
-    const TunedGeometry tg = tuned_geometry(w, a, N, ntiles, sms, strict, vec, st, run);
+    // Unaligned layouts (H*W % 4 != 0 or unaligned tensors): the coalesced-epilogue
+    // build is a candidate while its per-warp scratch fits next to the tile.
+    const bool coal_ok = !vec && w->knobs.coal != 0 && !acc_in && a.K_img == a.K &&
+                         smem_bytes(w->cols, (w->rows + 3) & ~3, w->T) +
+                                 16 * sizeof(float) * spcvk::coal_scratch_floats(w->G, w->T) <=
+                             kSmemLimit;
+    const TunedGeometry tg = tuned_geometry(w, a, N, ntiles, sms, strict, vec, coal_ok, st, run);
     a.tail_pref = tg.tail;
     a.split_pref = tg.split;
+    a.coal = tg.coal;
     return run(a);
 }
 

@@ -35,10 +35,11 @@ struct Knobs {
     int pass_k = 0;        // SPCV_PASS_K: run matrices wider than this as channel passes of this width
     int small = 1;         // SPCV_SMALL: 0 = never the few-column kernel, 2 = always (single pass)
     bool small_head = true;  // SPCV_SMALL_HEAD=0: no per-row head table for the few-column kernel
+    int coal = 1;          // SPCV_COAL: coalesced epilogue for unaligned layouts 0 = never, 1 = where the first call measures it faster, 2 = always
     int regcap = 1;        // SPCV_REGCAP=0: never the 80-register build of the unstructured 2-step kernels
     static Knobs from_env();
     long long geometry_key() const {
-        return ((static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1) * 2 + regcap;
+        return (((static_cast<long long>(nwarps) * 64 + split) * 64 + tail + 1) * 2 + regcap) * 4 + coal;
     }
 };
 
@@ -120,7 +121,7 @@ struct spcv_cu_weights {
     // channel order, each continuing the previous part's sums (spcv_cu.cu)
     std::vector<spcv_cu_weights*> parts;
     std::vector<int> part_k0;
-    // autotuned launch geometry per call shape: split * 64 + tail + 1 (spcv_cu.cu: tuned_geometry)
+    // autotuned launch geometry per call shape: coal * 4096 + split * 64 + tail + 1 (spcv_cu.cu: tuned_geometry)
     mutable std::mutex tune_mu;
     mutable std::vector<std::pair<long long, int>> tuned_tail;
 };

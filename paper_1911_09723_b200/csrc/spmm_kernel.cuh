@@ -66,9 +66,15 @@ struct KernelArgs {
     int steps;               // steps per chunk of `stream` (host-side dispatch)
     int tail_pref;           // host-side: tail split chosen by the autotuner (-1: heuristic, 0: none)
     int split_pref;          // host-side: CTAs per tile chosen by the autotuner (0: heuristic)
+    int coal;                // host-side: 1 = the coalesced epilogue build (unaligned layouts)
     // {1.0f, 1.0f} as f32x2, passed at run time so ptxas cannot fold the
     // strict pair mul.rn.f32x2 + fma.rn.f32x2(acc, one, p) into one FFMA2.
     unsigned long long one2;
+#ifdef SPCV_TIMELINE
+    // tools/timeline.py builds (make VARIANT=tl VFLAGS=-DSPCV_TIMELINE): per CTA
+    // {SM id, entry, tile staged, first / last warp done, exit} in globaltimer ns
+    unsigned long long* tl;
+#endif
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -205,14 +211,25 @@ constexpr int kHoist = SPCV_HOIST;  // steps of activation loads issued ahead of
 // ACC: a channel pass — activations of K_img channels per image, and (after
 // the first pass) accumulators starting at acc_in. A separate instantiation,
 // so the single-pass kernels carry none of its code.
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES = false, bool ACC = false>
+// COAL (unaligned layouts only, !VEC): the row group's outputs go through a
+// per-warp shared-memory scratch and are stored row by row, lane = column
+// (one or two contiguous segments per warp store instead of 32 scattered 4 B
+// pieces over G rows: the scattered form costs as many L1 wavefronts as the
+// whole gather once rows are short, e.g. H*W = 49 at >= 95 % sparsity).
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES = false, bool ACC = false,
+          bool COAL = false>
 struct Exec {
     static constexpr int G = 32 / LPR;
     static constexpr int T = LPR * NF * 4;
+    static constexpr int RS = T + 4;           // scratch row stride (floats): rows 16 B-aligned, banks shifted
+    static constexpr int CPL = (T + 31) / 32;  // columns per lane when lane = column
 
     float4 acc[BH][NF];
     uint32_t lane_off[NF];  // byte offset of this lane's j-th quad within a tile row
-    long long ocol[VEC ? NF : 1];  // VEC: output offset of each quad's first column
+    long long ocol[VEC ? NF : (COAL ? CPL : 1)];  // VEC: output offset of each quad's first column;
+                                                  // COAL: of columns lane, lane + 32, ...
+    float* s_out;           // COAL: this warp's scratch [G][RS]
+    int slot;               // this lane's row slot (lane / LPR)
     uint32_t brow;
     const char* s_bytes;    // current activation tile [K+1][T]
     const long long* s_col; // its output column offsets [T] (-1: past the end)
@@ -223,6 +240,7 @@ struct Exec {
 #pragma unroll
         for (int j = 0; j < NF; ++j)  // LPR >= 8: a phase is one row, no swizzle needed
             lane_off[j] = 16u * (li + LPR * (LPR >= 8 ? j : (j + gi) % NF));
+        slot = gi;
         brow = kNoRow;
         s_bias = bias_smem;
         have_bias = hb;
@@ -245,10 +263,62 @@ struct Exec {
         if constexpr (VEC) {
 #pragma unroll
             for (int j = 0; j < NF; ++j) ocol[j] = col_offset(n0 + (lane_off[j] >> 2), a);
+        } else if constexpr (COAL) {
+            const int lane = static_cast<int>(threadIdx.x) & 31;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) ocol[c] = lane + 32 * c < T ? s_col[lane + 32 * c] : -1;
         }
     }
 
+    // COAL epilogue: every lane of the warp takes part (empty slots write nothing).
+    __device__ __forceinline__ void finish_coalesced(const KernelArgs& a) {
+        const bool relu = a.act_kind == 1 && a.hi == __int_as_float(0x7f800000);  // clamp(lo, +inf)
+        const int lane = static_cast<int>(threadIdx.x) & 31;
+#pragma unroll
+        for (int i = 0; i < BH; ++i) {
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+                float4 v = acc[i][j];
+                if (relu) {
+                    v.x = clamp_lo(v.x, a.lo);
+                    v.y = clamp_lo(v.y, a.lo);
+                    v.z = clamp_lo(v.z, a.lo);
+                    v.w = clamp_lo(v.w, a.lo);
+                } else {
+                    v.x = clamp_ref(v.x, a.act_kind, a.lo, a.hi);
+                    v.y = clamp_ref(v.y, a.act_kind, a.lo, a.hi);
+                    v.z = clamp_ref(v.z, a.act_kind, a.lo, a.hi);
+                    v.w = clamp_ref(v.w, a.act_kind, a.lo, a.hi);
+                }
+                *reinterpret_cast<float4*>(s_out + slot * RS + (lane_off[j] >> 2)) = v;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint32_t br = __shfl_sync(0xffffffffu, brow, g * LPR);  // slot g's block row
+                const int r = static_cast<int>(br) * BH + i;
+                if (br == kNoRow || r >= a.M_out) continue;  // empty slot / padded row (never stored)
+                const long long roff = static_cast<long long>(r) * a.S;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const long long o = ocol[c];
+                    if (o >= 0) {
+                        float x = s_out[g * RS + lane + 32 * c];
+                        if constexpr (RES) x = __fadd_rn(x, __ldcs(a.residual + o + roff));
+                        __stcs(a.out + o + roff, x);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        brow = kNoRow;
+    }
+
     __device__ __forceinline__ void finish(const KernelArgs& a) {
+        if constexpr (!VEC && COAL) {
+            finish_coalesced(a);
+            return;
+        }
         if (brow == kNoRow) return;
         const bool relu = a.act_kind == 1 && a.hi == __int_as_float(0x7f800000);  // clamp(lo, +inf)
 #pragma unroll
@@ -495,6 +565,22 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
     }
 }
 
+// Per-warp scratch of the COAL epilogue: [G][T + 4] floats.
+__host__ __device__ constexpr int coal_scratch_floats(int G, int T) { return G * (T + 4); }
+
+#ifdef SPCV_TIMELINE
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(s));
+    return s;
+}
+#endif
+
 // ---------------------------------------------------------------- kernel 1
 // One tile per CTA; all threads stage it with cp.async (16 B when VEC).
 // CAP: compiled for three 8-warp CTAs per SM (at most 80 registers). ptxas
@@ -502,10 +588,11 @@ __device__ __forceinline__ void stage_tile(float* s_act, long long* s_col, long 
 // the K <= 512 layers to two CTAs per SM (measured: MBv1 pw5 237.6 vs 215.2 us,
 // pw7 215.1 vs 206.8 us); the 16-warp launches of wide tiles use CAP = false.
 constexpr int kCapThreads = 256, kCapBlocks = 3;
-template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false>
+template <int BH, int LPR, int NF, int STEPS, bool STRICT, bool VEC, bool RES, bool ACC = false, bool CAP = false,
+          bool COAL = false>
 __global__ void __launch_bounds__(CAP ? kCapThreads : kThreads, CAP ? kCapBlocks : kMinBlocks)
 spmm_bcsr_kernel(const KernelArgs a) {
-    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC>;
+    using E = Exec<BH, LPR, NF, STEPS, STRICT, VEC, RES, ACC, COAL>;
     constexpr int G = E::G;
     constexpr int T = E::T;
     constexpr int kRing = BH == 1 ? 3 : 2;  // weight-stream chunks in flight per warp
@@ -517,6 +604,15 @@ spmm_bcsr_kernel(const KernelArgs a) {
 
     const int tid = threadIdx.x;
     const int nthreads = blockDim.x;
+#ifdef SPCV_TIMELINE
+    unsigned long long* tl = a.tl ? a.tl + 8ull * (blockIdx.x + static_cast<unsigned long long>(gridDim.x) * blockIdx.y) : nullptr;
+    if (tl && tid == 0) {
+        tl[0] = smid();
+        tl[1] = gtime();
+        tl[3] = ~0ull;
+        tl[4] = 0;
+    }
+#endif
     // (tile, row part): full tiles first, then the tail tiles split tail_split ways
     long long tile = blockIdx.x;
     int part = blockIdx.y, nparts = gridDim.y;
@@ -558,11 +654,16 @@ spmm_bcsr_kernel(const KernelArgs a) {
 
     cp_async_wait_all();
     __syncthreads();
+#ifdef SPCV_TIMELINE
+    if (tl && tid == 0) tl[2] = gtime();
+#endif
 
     E ex;
     ex.init(gi, lane % LPR, s_bias, a.bias != nullptr);
     ex.s_bytes = reinterpret_cast<const char*>(s_act);
     ex.s_col = s_col;
+    if constexpr (COAL)  // per-warp output scratch after the bias (16 B-aligned)
+        ex.s_out = s_bias + ((a.M + 3) & ~3) + warp * coal_scratch_floats(G, T);
     ex.set_tile(n0, a);
 
     // Ring rotation by static unrolling: slot d always holds chunk pos+d at
@@ -580,6 +681,17 @@ spmm_bcsr_kernel(const KernelArgs a) {
     for (int d = 0; d < kRing; ++d)
         if (pos + d < end) ex.consume(ring[d], a);
     ex.finish(a);
+#ifdef SPCV_TIMELINE
+    if (tl) {
+        if ((tid & 31) == 0) {
+            const unsigned long long t = gtime();
+            atomicMin(tl + 3, t);
+            atomicMax(tl + 4, t);
+        }
+        __syncthreads();
+        if (tid == 0) tl[5] = gtime();
+    }
+#endif
 }
 
 }  // namespace spcvk

@@ -894,6 +894,44 @@ def test_bound_call_equals_direct_call(oracle):
         sp.bind_batched(dw, a.cpu(), b, act_of(layer.act), o)
 
 
+# ------------------------ unaligned layouts: coalesced epilogue (SPCV_COAL)
+@pytest.mark.parametrize("coal", ["0", "2", "1"], ids=["scattered", "coalesced", "autotuned"])
+@pytest.mark.parametrize("case", [
+    ("pw13", mbv1_pointwise()[12], 10),                                   # K = 1024: one 16-warp CTA per SM
+    ("c5_s98", Layer("c5", 1024, 1024, 7, 7, ("clamp", 0.0, float("inf")), -1.0, 1.0, 0.98, 1, True), 12),
+    ("mbv2_7x7", Layer("b15e", 160, 960, 7, 7, sparsity=0.85), 16),        # 64-column tiles
+    ("bh4_odd", Layer("bh4_odd", 96, 40, 5, 7, sparsity=0.7, block_h=4), 9),  # 4x1 blocks, 128-column tiles
+    ("bh2_pad", Layer("bh2_pad", 200, 22, 3, 3, sparsity=0.5, block_h=2), 5),
+], ids=lambda c: c[0])
+def test_unaligned_epilogues_bit_exact(oracle, monkeypatch, coal, case):
+    """H*W % 4 != 0: the scattered 4 B epilogue, the coalesced one (row group
+    through a per-warp shared-memory scratch, stored row by row) and the
+    autotuner's pick between them are bit-identical to the oracle, with and
+    without a residual and with padded rows truncated."""
+    import torch
+
+    use_kernel(monkeypatch, "tile")
+    monkeypatch.setenv("SPCV_COAL", coal)
+    if coal != "1":
+        monkeypatch.setenv("SPCV_AUTOTUNE", "0")
+    _, layer, images = case
+    d = make_layer_data(layer, images, 13)
+    dw = sp.DeviceBcsr(d.weights)
+    want = oracle.spmm(d.weights, d.act, d.bias, layer.act, nthreads=8)
+    for _ in range(2):
+        got = run_device(d.weights, d.act, d.bias, layer.act, dw=dw)
+        assert np.array_equal(bits(got), bits(want.reshape(got.shape)))
+    # executor step: logical rows < stored rows, residual added after the clamp
+    rows = layer.cout - (1 if layer.block_h > 1 else 0)
+    a = torch.from_numpy(d.act).cuda()
+    res = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (images, rows, layer.h, layer.w)).astype(np.float32)).cuda()
+    o = torch.full((images, rows, layer.h, layer.w), float("nan"), device="cuda")
+    sp.spmm_layer(dw, a, torch.from_numpy(d.bias[:rows].copy()).cuda(), act_of(layer.act), o, residual=res)
+    torch.cuda.synchronize()
+    w4 = want.reshape(images, layer.cout, layer.h, layer.w)[:, :rows]
+    assert np.array_equal(bits(o.cpu().numpy()), bits((w4 + res.cpu().numpy()).astype(np.float32)))
+
+
 # ------------------------------------ launch geometry: tail and row splits
 @pytest.mark.parametrize("env", [{"SPCV_TAIL": "0"}, {"SPCV_TAIL": "2"}, {"SPCV_TAIL": "4"}, {"SPCV_TAIL": "8"},
                                  {"SPCV_SPLIT": "2", "SPCV_TAIL": "4"}, {"SPCV_NWARPS": "8", "SPCV_TAIL": "8"},
