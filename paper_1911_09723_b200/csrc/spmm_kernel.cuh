@@ -634,23 +634,24 @@ spmm_bcsr_kernel(const KernelArgs a) {
 
     // ---- this warp's contiguous slice of the weight stream ----
     // V = warps/CTA x CTAs sharing the tile virtual warps; each owns kBins/V
-    // consecutive schedule bins (balanced by the packer's LPT at every split).
+    // consecutive schedule bins (balanced by the packer at every split level).
     const int per = kBins / ((nthreads >> 5) * nparts);
     const int bin0 = (part * (nthreads >> 5) + warp) * per;
     uint32_t pos = __ldg(a.bin_beg + bin0);
     const uint32_t end = __ldg(a.bin_beg + bin0 + per);
 
-    Chunk<BH, STEPS> ring[kRing];
-#pragma unroll
-    for (int d = 0; d < kRing; ++d)
-        ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + d, end, gi);
-
-    // ---- bias, column offsets and the [K][T] tile ----
+    // ---- bias, column offsets and the [K][T] tile: issued while the slice bounds are in flight
+    // (the ring's loads depend on them; the copies do not, and the volatile asms keep source order) ----
     if (a.bias != nullptr) {  // logical rows from bias; padded rows (never stored) get 0
         for (int i = tid; i < a.M_out; i += nthreads) cp_async4(s_bias + i, a.bias + i);
         for (int i = a.M_out + tid; i < a.M; i += nthreads) s_bias[i] = 0.0f;
     }
     stage_tile<T, VEC, ACC>(s_act, s_col, n0, a, tid, nthreads);
+
+    Chunk<BH, STEPS> ring[kRing];
+#pragma unroll
+    for (int d = 0; d < kRing; ++d)
+        ring[d] = ring_chunk<BH, G, STEPS>(a.stream, pos + d, end, gi);
 
     cp_async_wait_all();
     __syncthreads();
