@@ -1,5 +1,5 @@
 // launch.cuh — kernel selection and launch geometry, instantiated per block
-// height by launch_bh{1,2,4}.cu (parallel compilation).
+// height and staging width by launch_bh{1,2,4}.cu / launch_bh{1,2,4}u.cu (parallel compilation).
 #pragma once
 
 #include <algorithm>
@@ -98,38 +98,37 @@ int launch_one(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long n
                       : launch_one_r<BH, LPR, NF, STEPS, STRICT, VEC, false>(a, w, ntiles, sms, st);
 }
 
-template <int BH, int LPR, int NF, int STEPS>
+// VEC (16 B-aligned layouts) and !VEC kernels live in separate translation
+// units (launch_bh{1,2,4}.cu / launch_bh{1,2,4}u.cu): half the compile time each.
+template <int BH, int LPR, int NF, int STEPS, bool VEC>
 int launch_g(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
-             bool strict, bool vec, cudaStream_t st) {
-    if (strict)
-        return vec ? launch_one<BH, LPR, NF, STEPS, true, true>(a, w, nt, sms, st)
-                   : launch_one<BH, LPR, NF, STEPS, true, false>(a, w, nt, sms, st);
-    return vec ? launch_one<BH, LPR, NF, STEPS, false, true>(a, w, nt, sms, st)
-               : launch_one<BH, LPR, NF, STEPS, false, false>(a, w, nt, sms, st);
+             bool strict, cudaStream_t st) {
+    return strict ? launch_one<BH, LPR, NF, STEPS, true, VEC>(a, w, nt, sms, st)
+                  : launch_one<BH, LPR, NF, STEPS, false, VEC>(a, w, nt, sms, st);
 }
 
-template <int BH, int LPR, int NF>
+template <int BH, int LPR, int NF, bool VEC>
 int launch_s(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
-             bool strict, bool vec, cudaStream_t st) {
-    return a.steps == 2 ? launch_g<BH, LPR, NF, 2>(a, w, nt, sms, strict, vec, st)
-                         : launch_g<BH, LPR, NF, 4>(a, w, nt, sms, strict, vec, st);
+             bool strict, cudaStream_t st) {
+    return a.steps == 2 ? launch_g<BH, LPR, NF, 2, VEC>(a, w, nt, sms, strict, st)
+                         : launch_g<BH, LPR, NF, 4, VEC>(a, w, nt, sms, strict, st);
 }
 
-template <int BH>
+template <int BH, bool VEC>
 int launch_bh(const spcvk::KernelArgs& a, const spcv_cu_weights* w, long long nt, int sms,
-              bool strict, bool vec, cudaStream_t st) {
+              bool strict, cudaStream_t st) {
     if (BH == 4 || w->NF == 2) {
         switch (w->LPR) {
-            case 16: return launch_s<BH, 16, 2>(a, w, nt, sms, strict, vec, st);
-            case 8: return launch_s<BH, 8, 2>(a, w, nt, sms, strict, vec, st);
-            default: return launch_s<BH, 4, 2>(a, w, nt, sms, strict, vec, st);
+            case 16: return launch_s<BH, 16, 2, VEC>(a, w, nt, sms, strict, st);
+            case 8: return launch_s<BH, 8, 2, VEC>(a, w, nt, sms, strict, st);
+            default: return launch_s<BH, 4, 2, VEC>(a, w, nt, sms, strict, st);
         }
     }
     if constexpr (BH != 4) {
         switch (w->LPR) {
-            case 8: return launch_s<BH, 8, 4>(a, w, nt, sms, strict, vec, st);
-            case 4: return launch_s<BH, 4, 4>(a, w, nt, sms, strict, vec, st);
-            default: return launch_s<BH, 2, 4>(a, w, nt, sms, strict, vec, st);
+            case 8: return launch_s<BH, 8, 4, VEC>(a, w, nt, sms, strict, st);
+            case 4: return launch_s<BH, 4, 4, VEC>(a, w, nt, sms, strict, st);
+            default: return launch_s<BH, 2, 4, VEC>(a, w, nt, sms, strict, st);
         }
     }
     return fail(SPCV_ERR_UNSUPPORTED, "spmm: no kernel for this layout");
