@@ -48,6 +48,10 @@ __device__ __forceinline__ float madd_s(float acc, float w, float x) {
 }
 
 constexpr int kSmallWarps = 4;  // block rows per CTA (same column group)
+#ifndef SPCV_SMALL_NG
+#define SPCV_SMALL_NG 8
+#endif
+constexpr int kGathers = SPCV_SMALL_NG;  // activation gathers in flight per warp
 
 template <int BH, bool STRICT, bool RES>
 __global__ void __launch_bounds__(kSmallWarps * 32)
@@ -90,16 +94,16 @@ spmm_small_kernel(const SmallArgs a) {
     }
     for (uint32_t t0 = rb;;) {
         const uint32_t cnt = min(32u, re - t0);
-        // 8 gathers in flight, then their products, in stored order
-        for (uint32_t t = 0; t < cnt; t += 8) {
-            float x[8];
+        // kGathers gathers in flight, then their products, in stored order
+        for (uint32_t t = 0; t < cnt; t += kGathers) {
+            float x[kGathers];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kGathers; ++q) {
                 const int k = __shfl_sync(0xffffffffu, static_cast<int>(kcol), (t + q) & 31);
                 x[q] = (valid && t + q < cnt) ? __ldg(act + static_cast<long long>(k) * a.S) : 0.0f;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < kGathers; ++q) {
 #pragma unroll
                 for (int i = 0; i < BH; ++i) {
                     const float w = __shfl_sync(0xffffffffu, wv[i], (t + q) & 31);
